@@ -1,0 +1,137 @@
+/*
+ * sentinel_b200 -- C ABI of the B200 hashing engine.
+ *
+ * The reference (`sentinel`, /root/reference/pkg/src/sentinel) is pure Python
+ * and has no FFI seam of its own; its drop-in boundary is the function API
+ * re-exported in __init__.py:3-43. Each entry point below is what a binding
+ * for one of those functions calls. All pointers named d_* are DEVICE
+ * pointers; everything else is host memory. Every launch goes to the
+ * caller's stream and nothing synchronises unless stated. The library never
+ * owns caller memory and keeps no mutable global state.
+ *
+ * Return value: 0 on success, a negative snt_status otherwise. No C++
+ * exception crosses this boundary. The Python package maps the codes onto the
+ * reference's exception classes (errors.py:4-33).
+ */
+#ifndef SENTINEL_B200_H
+#define SENTINEL_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* cudaStream_t without pulling in the CUDA headers. */
+typedef void* snt_stream_t;
+
+typedef enum snt_status {
+    SNT_OK = 0,
+    SNT_ERR_INVALID_INPUT = -1, /* errors.py:8  InvalidInput  (empty model, zero blocks) */
+    SNT_ERR_INVALID_STATE = -2, /* errors.py:12 InvalidState  (reduce_level on < 2 digests) */
+    SNT_ERR_CONFIG = -3,        /* errors.py:16 ConfigError   (bad block size / algorithm) */
+    SNT_ERR_VALIDATION = -4,    /* errors.py:24 ValidationError */
+    SNT_ERR_RESOURCE = -5       /* errors.py:28 ResourceError (CUDA failure, workspace too small) */
+} snt_status;
+
+/* compression.py:19-22 CompressionAlg; digest lengths compression.py:39-43. */
+typedef enum snt_alg { SNT_SHA256 = 0, SNT_BLAKE2B = 1, SNT_SHA3_256 = 2 } snt_alg;
+
+#define SNT_LEVELS_TO_ROOT 0xffffffffu
+
+const char* snt_strerror(int status);
+/* Last CUDA error string seen by this thread's failing call (diagnostics). */
+const char* snt_last_cuda_error(void);
+uint32_t snt_abi_version(void);
+/* 32, 64, 32 -- or 0 for an unknown algorithm. */
+uint32_t snt_digest_len(int alg);
+
+/* ---- model block table ---------------------------------------------------
+ * Replaces BlockTable.build (model.py:137-146): a per-tensor table
+ * (address, byte length, first leaf index) kept on the device, searched by
+ * the kernels. Empty tensors own no leaves; the last leaf of a tensor is
+ * hashed at its true length. Creating a plan allocates one small device
+ * buffer and synchronises once; hashing calls never allocate.
+ */
+typedef struct snt_model_plan snt_model_plan;
+
+int snt_model_plan_create(const void* const* d_tensor_ptrs, const uint64_t* tensor_nbytes,
+                          uint32_t n_tensors, uint32_t block_size, snt_model_plan** out_plan);
+void snt_model_plan_destroy(snt_model_plan* plan);
+uint64_t snt_model_plan_leaf_count(const snt_model_plan* plan);
+uint64_t snt_model_plan_total_bytes(const snt_model_plan* plan);
+
+/* Bytes of scratch snt_merkle_inplace / snt_merkle_root need for `count`
+ * input digests of `alg`. */
+size_t snt_merkle_work_bytes(int alg, uint64_t count);
+
+/* inplace_hash, MERKLE construction (model.py:298-310): hash leaves
+ * [leaf_begin, leaf_end) of the plan and reduce them `levels` tree levels.
+ *   levels = SNT_LEVELS_TO_ROOT with the full range: d_out receives the root
+ *   (for a one-leaf model, the leaf itself -- merkle.py:159-160).
+ *   levels = k with leaf_begin a multiple of 2^k and leaf_end a multiple of
+ *   2^k or the leaf count: d_out receives the ceil((end-begin)/2^k) level-k
+ *   nodes of that range (multi-GPU sharding; nodes combine with
+ *   snt_merkle_root / snt_merkle_reduce_levels into the reference root).
+ * d_leaves (may not be NULL) receives every leaf digest of the range.
+ */
+int snt_merkle_inplace(const snt_model_plan* plan, int alg, uint64_t leaf_begin,
+                       uint64_t leaf_end, uint32_t levels, void* d_leaves, void* d_work,
+                       size_t work_bytes, void* d_out, snt_stream_t stream);
+
+/* hash_blocks (merkle.py:93-114): d_out[i] = H(d_base[d_off[i] .. +d_len[i]]).
+ * Blocks may be empty, ragged and unaligned. n == 0 -> SNT_ERR_INVALID_INPUT. */
+int snt_hash_blocks(int alg, const void* d_base, const uint64_t* d_off, const uint64_t* d_len,
+                    uint64_t n, void* d_out, snt_stream_t stream);
+
+/* reduce_level (merkle.py:117-149) generalised to `levels` consecutive
+ * levels over the node range [first, first + n_in) of a level that has
+ * `level_count` nodes in the whole tree. first must be a multiple of
+ * 2^levels; first + n_in must be level_count or a multiple of 2^levels.
+ * Writes ceil(n_in / 2^levels) nodes. An odd level pairs its last node with
+ * zero bytes; levels are never skipped. d_out must not alias d_in. */
+int snt_merkle_reduce_levels(int alg, const void* d_in, uint64_t first, uint64_t n_in,
+                             uint64_t level_count, uint32_t levels, void* d_work,
+                             size_t work_bytes, void* d_out, snt_stream_t stream);
+
+/* merkle_root (merkle.py:152-165): count == 1 copies the leaf;
+ * count == 0 -> SNT_ERR_INVALID_INPUT. d_nodes is not modified. */
+int snt_merkle_root(int alg, const void* d_nodes, uint64_t count, void* d_work, size_t work_bytes,
+                    void* d_root, snt_stream_t stream);
+
+/* ---- LtHash ------------------------------------------------------------------
+ * Accumulators are n_sources x 32 u32 lanes (sums modulo 2^32 of the u16
+ * lanes; exact modulo 2^16 after snt_lt_finalize) plus n_sources u64 counts.
+ * Calls ADD into d_acc / d_counts (zero them first for a fresh digest), so
+ * batches stream through the same accumulators (SourceAccumulator,
+ * dataset.py:52-71) and partial accumulators from several GPUs combine with
+ * one u32 sum all-reduce.
+ */
+
+/* process_batch / hash_sample (dataset.py:41-49, :74-86): sample i is
+ * d_shard[d_off[i] .. +d_len[i]], digest BLAKE2b-512(LE64(d_ids[i]) || sample),
+ * added into source slot d_slot[i]. A slot >= n_sources sets bit 0 of
+ * *d_status (if not NULL) and the sample is skipped (undeclared source).
+ * d_digests, if not NULL, receives the n x 64 per-sample digests. */
+int snt_lthash_samples(const void* d_shard, const uint64_t* d_off, const uint64_t* d_len,
+                       const uint64_t* d_ids, const uint32_t* d_slot, uint64_t n,
+                       uint32_t n_sources, uint32_t* d_acc, uint64_t* d_counts, void* d_digests,
+                       uint32_t* d_status, snt_stream_t stream);
+
+/* inplace_hash, LATTICE construction (model.py:312-315): leaves
+ * [leaf_begin, leaf_end) tagged LE64(k), summed into d_acc[32] / d_counts[1]. */
+int snt_lthash_model(const snt_model_plan* plan, uint64_t leaf_begin, uint64_t leaf_end,
+                     uint32_t* d_acc, uint64_t* d_counts, void* d_digests, snt_stream_t stream);
+
+/* lt_reduce (lattice.py:104-119): add n 64-byte digests into d_acc[32]. */
+int snt_lt_reduce(const void* d_digests, uint64_t n, uint32_t* d_acc, snt_stream_t stream);
+
+/* Mask to 16 bits and pack: d_out receives n_sources x 64 bytes
+ * (LatticeDigest layout, lattice.py:37-58). */
+int snt_lt_finalize(const uint32_t* d_acc, uint32_t n_sources, void* d_out, snt_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SENTINEL_B200_H */

@@ -1,0 +1,381 @@
+// C ABI of the B200 hashing engine (see include/sentinel_b200.h).
+// Host-side orchestration only: argument checks, launch geometry, the chain of
+// level-reducer launches. No torch types, no allocation on the hashing path.
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "../../include/sentinel_b200.h"
+#include "lthash_kernels.cuh"
+#include "merkle_kernels.cuh"
+
+using namespace snt;
+
+namespace {
+
+thread_local char g_cuda_err[256] = "";
+
+int cuda_fail(cudaError_t e, const char* where) {
+    snprintf(g_cuda_err, sizeof(g_cuda_err), "%s: %s", where, cudaGetErrorString(e));
+    return SNT_ERR_RESOURCE;
+}
+
+#define SNT_CUDA(call)                                        \
+    do {                                                      \
+        cudaError_t e__ = (call);                             \
+        if (e__ != cudaSuccess) return cuda_fail(e__, #call); \
+    } while (0)
+
+uint32_t ceil_log2(uint64_t n) {
+    uint32_t l = 0;
+    while ((1ull << l) < n) ++l;
+    return l;
+}
+
+uint64_t cdiv_shift(uint64_t n, uint32_t s) { return ceil_shift(n, s); }
+
+bool valid_alg(int alg) { return alg == SNT_SHA256 || alg == SNT_BLAKE2B || alg == SNT_SHA3_256; }
+
+const MerkleConsts& node_consts() {
+    static const MerkleConsts c = [] {
+        MerkleConsts k;
+        memset(&k, 0, sizeof(k));
+        Sha256::pad_schedule(64, k.sha256_pad_node);
+        return k;
+    }();
+    return c;
+}
+
+}  // namespace
+
+struct snt_model_plan {
+    uint64_t* d_table = nullptr;     // addr[n] | nbytes[n] | first_leaf[n + 1]
+    uint32_t n_tensors = 0;
+    uint32_t block_shift = 0;
+    uint64_t n_leaves = 0;
+    uint64_t total_bytes = 0;
+    MerkleConsts consts;
+    TensorTable table() const {
+        TensorTable t;
+        t.addr = d_table;
+        t.nbytes = d_table + n_tensors;
+        t.first_leaf = d_table + 2ull * n_tensors;
+        t.n_tensors = n_tensors;
+        t.block_shift = block_shift;
+        t.n_leaves = n_leaves;
+        return t;
+    }
+};
+
+extern "C" {
+
+const char* snt_strerror(int status) {
+    switch (status) {
+        case SNT_OK: return "ok";
+        case SNT_ERR_INVALID_INPUT: return "invalid input";
+        case SNT_ERR_INVALID_STATE: return "invalid state";
+        case SNT_ERR_CONFIG: return "bad hashing configuration";
+        case SNT_ERR_VALIDATION: return "validation failed";
+        case SNT_ERR_RESOURCE: return "CUDA resource error";
+        default: return "unknown status";
+    }
+}
+
+const char* snt_last_cuda_error(void) { return g_cuda_err; }
+
+uint32_t snt_abi_version(void) { return 1; }
+
+uint32_t snt_digest_len(int alg) {
+    switch (alg) {
+        case SNT_SHA256: return 32;
+        case SNT_BLAKE2B: return 64;
+        case SNT_SHA3_256: return 32;
+        default: return 0;
+    }
+}
+
+int snt_model_plan_create(const void* const* d_tensor_ptrs, const uint64_t* tensor_nbytes,
+                          uint32_t n_tensors, uint32_t block_size, snt_model_plan** out_plan) {
+    if (!out_plan) return SNT_ERR_INVALID_INPUT;
+    *out_plan = nullptr;
+    if (block_size < 64 || (block_size & (block_size - 1))) return SNT_ERR_CONFIG;   // model.py:94-95
+    if (n_tensors == 0 || !d_tensor_ptrs || !tensor_nbytes) return SNT_ERR_INVALID_INPUT;
+    uint32_t shift = 0;
+    while ((1u << shift) < block_size) ++shift;
+    std::vector<uint64_t> host(3ull * n_tensors + 1);
+    uint64_t leaves = 0, total = 0;
+    for (uint32_t t = 0; t < n_tensors; ++t) {
+        host[t] = reinterpret_cast<uint64_t>(d_tensor_ptrs[t]);
+        host[n_tensors + t] = tensor_nbytes[t];
+        host[2ull * n_tensors + t] = leaves;
+        leaves += (tensor_nbytes[t] + block_size - 1) >> shift;
+        total += tensor_nbytes[t];
+        if (tensor_nbytes[t] && !d_tensor_ptrs[t]) return SNT_ERR_INVALID_INPUT;
+    }
+    host[3ull * n_tensors] = leaves;
+    if (total == 0) return SNT_ERR_INVALID_INPUT;                                     // model.py:166-168
+    snt_model_plan* p = new (std::nothrow) snt_model_plan();
+    if (!p) return SNT_ERR_RESOURCE;
+    p->n_tensors = n_tensors;
+    p->block_shift = shift;
+    p->n_leaves = leaves;
+    p->total_bytes = total;
+    p->consts = node_consts();
+    Sha256::pad_schedule(block_size, p->consts.sha256_pad_leaf);
+    cudaError_t e = cudaMalloc(&p->d_table, host.size() * sizeof(uint64_t));
+    if (e == cudaSuccess)
+        e = cudaMemcpy(p->d_table, host.data(), host.size() * sizeof(uint64_t), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+        if (p->d_table) cudaFree(p->d_table);
+        delete p;
+        return cuda_fail(e, "snt_model_plan_create");
+    }
+    *out_plan = p;
+    return SNT_OK;
+}
+
+void snt_model_plan_destroy(snt_model_plan* plan) {
+    if (!plan) return;
+    if (plan->d_table) cudaFree(plan->d_table);
+    delete plan;
+}
+
+uint64_t snt_model_plan_leaf_count(const snt_model_plan* plan) { return plan ? plan->n_leaves : 0; }
+uint64_t snt_model_plan_total_bytes(const snt_model_plan* plan) { return plan ? plan->total_bytes : 0; }
+
+size_t snt_merkle_work_bytes(int alg, uint64_t count) {
+    // two ping-pong buffers, each able to hold the widest intermediate level:
+    // every launch but the last folds REDUCE_MAX_LEVELS levels, so the widest
+    // intermediate has ceil(count / 2^REDUCE_MAX_LEVELS) nodes
+    return 2 * static_cast<size_t>(cdiv_shift(count, REDUCE_MAX_LEVELS) + 1) * snt_digest_len(alg);
+}
+
+}  // extern "C"
+
+namespace {
+
+template <int ALG>
+int launch_reduce(const uint8_t* in, uint64_t first, uint64_t n_in, uint64_t level_count,
+                  uint32_t levels, const MerkleConsts& c, uint8_t* out, cudaStream_t s) {
+    const uint64_t n_out = cdiv_shift(n_in, levels);
+    if (n_out > 0x7fffffffull) return SNT_ERR_INVALID_INPUT;
+    merkle_reduce_kernel<ALG><<<static_cast<unsigned>(n_out), REDUCE_THREADS, 0, s>>>(
+        in, first, n_in, level_count, levels, c, out);
+    SNT_CUDA(cudaGetLastError());
+    return SNT_OK;
+}
+
+int launch_reduce_alg(int alg, const uint8_t* in, uint64_t first, uint64_t n_in, uint64_t level_count,
+                      uint32_t levels, const MerkleConsts& c, uint8_t* out, cudaStream_t s) {
+    switch (alg) {
+        case SNT_SHA256: return launch_reduce<ALG_SHA256>(in, first, n_in, level_count, levels, c, out, s);
+        case SNT_BLAKE2B: return launch_reduce<ALG_BLAKE2B>(in, first, n_in, level_count, levels, c, out, s);
+        default: return launch_reduce<ALG_SHA3_256>(in, first, n_in, level_count, levels, c, out, s);
+    }
+}
+
+// Apply `levels` levels to the node range, REDUCE_MAX_LEVELS at a time,
+// ping-ponging intermediates through `work`; the last launch writes `out`.
+int reduce_chain(int alg, const uint8_t* in, uint64_t first, uint64_t n_in, uint64_t level_count,
+                 uint32_t levels, uint8_t* work, size_t work_bytes, uint8_t* out,
+                 const MerkleConsts& c, cudaStream_t s) {
+    const uint32_t dlen = snt_digest_len(alg);
+    const size_t half = work_bytes / 2;
+    int flip = 0;
+    const uint8_t* src = in;
+    while (levels > 0) {
+        const uint32_t m = levels < static_cast<uint32_t>(REDUCE_MAX_LEVELS) ? levels : REDUCE_MAX_LEVELS;
+        const uint64_t n_out = cdiv_shift(n_in, m);
+        uint8_t* dst = out;
+        if (levels > m) {
+            if (!work || n_out * dlen > half) return SNT_ERR_RESOURCE;
+            dst = work + (flip ? half : 0);
+            flip ^= 1;
+        }
+        const int rc = launch_reduce_alg(alg, src, first, n_in, level_count, m, c, dst, s);
+        if (rc != SNT_OK) return rc;
+        src = dst;
+        first >>= m;
+        n_in = n_out;
+        level_count = cdiv_shift(level_count, m);
+        levels -= m;
+    }
+    return SNT_OK;
+}
+
+template <int ALG>
+int launch_leaves(const snt_model_plan* plan, uint64_t begin, uint64_t end, uint8_t* d_leaves,
+                  cudaStream_t s) {
+    const uint64_t n = end - begin;
+    const uint64_t grid = (n + LEAF_THREADS - 1) / LEAF_THREADS;
+    if (grid > 0x7fffffffull) return SNT_ERR_INVALID_INPUT;
+    merkle_leaf_kernel<ALG><<<static_cast<unsigned>(grid), LEAF_THREADS, 0, s>>>(
+        plan->table(), plan->consts, begin, end, d_leaves);
+    SNT_CUDA(cudaGetLastError());
+    return SNT_OK;
+}
+
+template <int ALG>
+int launch_blocks(const uint8_t* base, const uint64_t* off, const uint64_t* len, uint64_t n,
+                  uint8_t* out, cudaStream_t s) {
+    const uint64_t grid = (n + LEAF_THREADS - 1) / LEAF_THREADS;
+    if (grid > 0x7fffffffull) return SNT_ERR_INVALID_INPUT;
+    hash_blocks_kernel<ALG><<<static_cast<unsigned>(grid), LEAF_THREADS, 0, s>>>(base, off, len, n, out);
+    SNT_CUDA(cudaGetLastError());
+    return SNT_OK;
+}
+
+template <class Items>
+int launch_lthash(const Items& items, uint64_t n, uint32_t n_sources, uint32_t* d_acc,
+                  uint64_t* d_counts, void* d_digests, uint32_t* d_status, cudaStream_t s) {
+    if (n == 0) return SNT_OK;
+    const uint64_t grid = (n + LT_THREADS - 1) / LT_THREADS;
+    if (grid > 0x7fffffffull) return SNT_ERR_INVALID_INPUT;
+    auto* counts = reinterpret_cast<unsigned long long*>(d_counts);
+    auto* dig = static_cast<uint8_t*>(d_digests);
+    if (n_sources <= static_cast<uint32_t>(LT_SMEM_SOURCES)) {
+        const size_t smem = static_cast<size_t>(n_sources) * (LT_LANES + 1) * sizeof(uint32_t);
+        lthash_kernel<Items, true><<<static_cast<unsigned>(grid), LT_THREADS, smem, s>>>(
+            items, n, n_sources, d_acc, counts, dig, d_status);
+    } else {
+        lthash_kernel<Items, false><<<static_cast<unsigned>(grid), LT_THREADS, 0, s>>>(
+            items, n, n_sources, d_acc, counts, dig, d_status);
+    }
+    SNT_CUDA(cudaGetLastError());
+    return SNT_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int snt_merkle_inplace(const snt_model_plan* plan, int alg, uint64_t leaf_begin, uint64_t leaf_end,
+                       uint32_t levels, void* d_leaves, void* d_work, size_t work_bytes, void* d_out,
+                       snt_stream_t stream) {
+    if (!plan || !d_leaves || !d_out) return SNT_ERR_INVALID_INPUT;
+    if (!valid_alg(alg)) return SNT_ERR_CONFIG;
+    const uint64_t n = plan->n_leaves;
+    if (leaf_begin >= leaf_end || leaf_end > n) return SNT_ERR_INVALID_INPUT;
+    if (levels == SNT_LEVELS_TO_ROOT) {
+        if (leaf_begin != 0 || leaf_end != n) return SNT_ERR_INVALID_INPUT;
+        levels = ceil_log2(n);
+    } else {
+        if (levels > 63) return SNT_ERR_INVALID_INPUT;
+        const uint64_t mask = (1ull << levels) - 1;
+        if ((leaf_begin & mask) || ((leaf_end & mask) && leaf_end != n)) return SNT_ERR_INVALID_INPUT;
+    }
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    uint8_t* leaves = static_cast<uint8_t*>(d_leaves);
+    int rc;
+    switch (alg) {
+        case SNT_SHA256: rc = launch_leaves<ALG_SHA256>(plan, leaf_begin, leaf_end, leaves, s); break;
+        case SNT_BLAKE2B: rc = launch_leaves<ALG_BLAKE2B>(plan, leaf_begin, leaf_end, leaves, s); break;
+        default: rc = launch_leaves<ALG_SHA3_256>(plan, leaf_begin, leaf_end, leaves, s); break;
+    }
+    if (rc != SNT_OK) return rc;
+    const uint32_t dlen = snt_digest_len(alg);
+    if (levels == 0) {
+        SNT_CUDA(cudaMemcpyAsync(d_out, leaves, static_cast<size_t>(leaf_end - leaf_begin) * dlen,
+                                 cudaMemcpyDeviceToDevice, s));
+        return SNT_OK;
+    }
+    return reduce_chain(alg, leaves, leaf_begin, leaf_end - leaf_begin, n, levels,
+                        static_cast<uint8_t*>(d_work), work_bytes, static_cast<uint8_t*>(d_out),
+                        plan->consts, s);
+}
+
+int snt_hash_blocks(int alg, const void* d_base, const uint64_t* d_off, const uint64_t* d_len, uint64_t n,
+                    void* d_out, snt_stream_t stream) {
+    if (!valid_alg(alg)) return SNT_ERR_CONFIG;
+    if (n == 0 || !d_off || !d_len || !d_out) return SNT_ERR_INVALID_INPUT;          // merkle.py:100-101
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const uint8_t* base = static_cast<const uint8_t*>(d_base);
+    uint8_t* out = static_cast<uint8_t*>(d_out);
+    switch (alg) {
+        case SNT_SHA256: return launch_blocks<ALG_SHA256>(base, d_off, d_len, n, out, s);
+        case SNT_BLAKE2B: return launch_blocks<ALG_BLAKE2B>(base, d_off, d_len, n, out, s);
+        default: return launch_blocks<ALG_SHA3_256>(base, d_off, d_len, n, out, s);
+    }
+}
+
+int snt_merkle_reduce_levels(int alg, const void* d_in, uint64_t first, uint64_t n_in, uint64_t level_count,
+                             uint32_t levels, void* d_work, size_t work_bytes, void* d_out,
+                             snt_stream_t stream) {
+    if (!valid_alg(alg)) return SNT_ERR_CONFIG;
+    if (!d_in || !d_out || n_in == 0 || levels == 0 || levels > 63) return SNT_ERR_INVALID_INPUT;
+    if (level_count < 2 && levels == 1 && first == 0 && n_in == level_count)
+        return SNT_ERR_INVALID_STATE;                                                 // merkle.py:125-126
+    const uint64_t mask = (1ull << levels) - 1;
+    const uint64_t end = first + n_in;
+    if ((first & mask) || end > level_count || ((end & mask) && end != level_count))
+        return SNT_ERR_INVALID_INPUT;
+    return reduce_chain(alg, static_cast<const uint8_t*>(d_in), first, n_in, level_count, levels,
+                        static_cast<uint8_t*>(d_work), work_bytes, static_cast<uint8_t*>(d_out),
+                        node_consts(), static_cast<cudaStream_t>(stream));
+}
+
+int snt_merkle_root(int alg, const void* d_nodes, uint64_t count, void* d_work, size_t work_bytes,
+                    void* d_root, snt_stream_t stream) {
+    if (!valid_alg(alg)) return SNT_ERR_CONFIG;
+    if (count == 0 || !d_nodes || !d_root) return SNT_ERR_INVALID_INPUT;              // merkle.py:156-157
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (count == 1) {                                                                 // merkle.py:159-160
+        SNT_CUDA(cudaMemcpyAsync(d_root, d_nodes, snt_digest_len(alg), cudaMemcpyDeviceToDevice, s));
+        return SNT_OK;
+    }
+    return reduce_chain(alg, static_cast<const uint8_t*>(d_nodes), 0, count, count, ceil_log2(count),
+                        static_cast<uint8_t*>(d_work), work_bytes, static_cast<uint8_t*>(d_root),
+                        node_consts(), s);
+}
+
+int snt_lthash_samples(const void* d_shard, const uint64_t* d_off, const uint64_t* d_len,
+                       const uint64_t* d_ids, const uint32_t* d_slot, uint64_t n, uint32_t n_sources,
+                       uint32_t* d_acc, uint64_t* d_counts, void* d_digests, uint32_t* d_status,
+                       snt_stream_t stream) {
+    if (n_sources == 0 || !d_acc || !d_counts) return SNT_ERR_INVALID_INPUT;
+    if (n && (!d_off || !d_len || !d_ids || !d_slot)) return SNT_ERR_INVALID_INPUT;
+    SampleItems items;
+    items.shard = static_cast<const uint8_t*>(d_shard);
+    items.off = d_off;
+    items.len = d_len;
+    items.ids = d_ids;
+    items.slot = d_slot;
+    return launch_lthash(items, n, n_sources, d_acc, d_counts, d_digests, d_status,
+                         static_cast<cudaStream_t>(stream));
+}
+
+int snt_lthash_model(const snt_model_plan* plan, uint64_t leaf_begin, uint64_t leaf_end, uint32_t* d_acc,
+                     uint64_t* d_counts, void* d_digests, snt_stream_t stream) {
+    if (!plan || !d_acc || !d_counts) return SNT_ERR_INVALID_INPUT;
+    if (leaf_begin > leaf_end || leaf_end > plan->n_leaves) return SNT_ERR_INVALID_INPUT;
+    LeafItems items;
+    items.tab = plan->table();
+    items.leaf_begin = leaf_begin;
+    return launch_lthash(items, leaf_end - leaf_begin, 1, d_acc, d_counts, d_digests, nullptr,
+                         static_cast<cudaStream_t>(stream));
+}
+
+int snt_lt_reduce(const void* d_digests, uint64_t n, uint32_t* d_acc, snt_stream_t stream) {
+    if (!d_acc || (n && !d_digests)) return SNT_ERR_INVALID_INPUT;
+    if (n == 0) return SNT_OK;                                                        // lattice.py:112-113
+    uint64_t grid = (n + 63) / 64;
+    if (grid > 148 * 8) grid = 148 * 8;
+    lt_reduce_kernel<<<static_cast<unsigned>(grid), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        static_cast<const uint8_t*>(d_digests), n, d_acc);
+    SNT_CUDA(cudaGetLastError());
+    return SNT_OK;
+}
+
+int snt_lt_finalize(const uint32_t* d_acc, uint32_t n_sources, void* d_out, snt_stream_t stream) {
+    if (!d_acc || !d_out || n_sources == 0) return SNT_ERR_INVALID_INPUT;
+    const uint32_t n_words = n_sources * (LT_LANES / 2);
+    lt_finalize_kernel<<<(n_words + 255) / 256, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        d_acc, n_words, static_cast<uint32_t*>(d_out));
+    SNT_CUDA(cudaGetLastError());
+    return SNT_OK;
+}
+
+}  // extern "C"

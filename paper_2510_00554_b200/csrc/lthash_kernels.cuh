@@ -1,0 +1,164 @@
+// LtHash kernels: BLAKE2b-512 of (index tag || bytes) per item, the 64 digest
+// bytes read as 32 little-endian u16 lanes, lanes summed per source modulo
+// 2^16. Sums are carried in u32 (exact modulo 2^32, masked to 16 bits at the
+// end), first in shared memory per CTA, then folded into the global
+// accumulator.
+//
+// Reference behaviour reproduced:
+//   lattice.py:92-101   lt_hash_block / lt_hash_tagged
+//   lattice.py:69-82    lt_add (per-lane add mod 2^16), :104-119 lt_reduce
+//   dataset.py:41-49    hash_sample, :74-86 process_batch (group by source, sum)
+//   model.py:183-193    _lattice_sum_blocks with tag LE64(k) (model.py:312)
+#pragma once
+#include "algs.cuh"
+
+namespace snt {
+
+constexpr int LT_THREADS = 64;
+constexpr int LT_LANES = 32;                 // u16 lanes per digest
+constexpr int LT_SMEM_SOURCES = 128;         // per-CTA shared accumulators: 128 x 32 x 4 B = 16 KiB
+
+struct LtItem {
+    const uint8_t* ptr;
+    uint64_t len;
+    uint64_t tag;
+    uint32_t slot;
+};
+
+// Dataset samples: a flat shard plus (offset, length, sample_id, source slot)
+// rows -- the manifest layout of dataset.py:94-100 moved to device arrays.
+struct SampleItems {
+    const uint8_t* __restrict__ shard;
+    const uint64_t* __restrict__ off;
+    const uint64_t* __restrict__ len;
+    const uint64_t* __restrict__ ids;
+    const uint32_t* __restrict__ slot;
+    SNT_HD LtItem get(uint64_t i) const {
+        LtItem it;
+        it.ptr = shard + off[i];
+        it.len = len[i];
+        it.tag = ids[i];
+        it.slot = slot[i];
+        return it;
+    }
+};
+
+// Model blocks hashed in place: item i is leaf k = leaf_begin + i of the block
+// table, tagged with the global block counter k (model.py:312).
+struct LeafItems {
+    TensorTable tab;
+    uint64_t leaf_begin;
+    SNT_HD LtItem get(uint64_t i) const {
+        const uint64_t k = leaf_begin + i;
+        const LeafRef r = locate_leaf(tab, k);
+        LtItem it;
+        it.ptr = r.ptr;
+        it.len = r.len;
+        it.tag = k;
+        it.slot = 0;
+        return it;
+    }
+};
+
+template <class Items, bool SMEM_ACC>
+__global__ void __launch_bounds__(LT_THREADS)
+lthash_kernel(const Items items, uint64_t n, uint32_t n_sources, uint32_t* __restrict__ acc,
+              unsigned long long* __restrict__ counts, uint8_t* __restrict__ digests,
+              uint32_t* __restrict__ status) {
+    extern __shared__ uint32_t sacc[];       // [n_sources][32] lanes, then [n_sources] counts
+    uint32_t* scnt = sacc + static_cast<size_t>(n_sources) * LT_LANES;
+    if (SMEM_ACC) {
+        for (uint32_t i = threadIdx.x; i < n_sources * (LT_LANES + 1); i += LT_THREADS) sacc[i] = 0;
+        __syncthreads();
+    }
+    const uint64_t i = static_cast<uint64_t>(blockIdx.x) * LT_THREADS + threadIdx.x;
+    if (i < n) {
+        const LtItem it = items.get(i);
+        if (it.slot >= n_sources) {
+            if (status) atomicOr(status, 1u);          // undeclared source (dataset.py:78-80)
+        } else {
+            uint64_t h[8];
+            Blake2b::hash_message<1>(it.tag, 0, it.ptr, it.len, h);
+            if (digests) {
+                uint4* o = reinterpret_cast<uint4*>(digests + i * 64);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    o[q] = make_uint4(static_cast<uint32_t>(h[2 * q]), static_cast<uint32_t>(h[2 * q] >> 32),
+                                      static_cast<uint32_t>(h[2 * q + 1]), static_cast<uint32_t>(h[2 * q + 1] >> 32));
+                }
+            }
+            uint32_t* dst = SMEM_ACC ? sacc + static_cast<size_t>(it.slot) * LT_LANES
+                                     : acc + static_cast<size_t>(it.slot) * LT_LANES;
+            // rotate the lane order by the thread's lane id: at every step the
+            // 32 threads of a warp hit 32 different shared-memory banks
+            // whatever their sources are.
+            const uint32_t rot = threadIdx.x & 31;
+#pragma unroll
+            for (int l = 0; l < LT_LANES; ++l) {
+                const uint32_t lane = (l + rot) & 31;
+                // u16 lane number (lane & 3) of 64-bit word (lane >> 2); the word is
+                // picked with a select chain because h[] lives in registers
+                uint64_t w = h[0];
+#pragma unroll
+                for (int q = 1; q < 8; ++q) w = (lane >> 2) == static_cast<uint32_t>(q) ? h[q] : w;
+                const uint32_t v = static_cast<uint32_t>(w >> (16 * (lane & 3))) & 0xffffu;
+                atomicAdd(dst + lane, v);
+            }
+            if (SMEM_ACC) atomicAdd(scnt + it.slot, 1u);
+            else atomicAdd(counts + it.slot, 1ull);
+        }
+    }
+    if (SMEM_ACC) {
+        __syncthreads();
+        for (uint32_t j = threadIdx.x; j < n_sources * LT_LANES; j += LT_THREADS) {
+            const uint32_t v = sacc[j];
+            if (v) atomicAdd(acc + j, v);
+        }
+        for (uint32_t j = threadIdx.x; j < n_sources; j += LT_THREADS) {
+            const uint32_t v = scnt[j];
+            if (v) atomicAdd(counts + j, static_cast<unsigned long long>(v));
+        }
+    }
+}
+
+// lt_reduce (lattice.py:104-119): sum n 64-byte digests into acc[32].
+__global__ void __launch_bounds__(256)
+lt_reduce_kernel(const uint8_t* __restrict__ digests, uint64_t n, uint32_t* __restrict__ acc) {
+    __shared__ uint32_t sacc[LT_LANES];
+    if (threadIdx.x < LT_LANES) sacc[threadIdx.x] = 0;
+    __syncthreads();
+    // thread (j, q): 16-byte quarter q of digest j -> 8 lanes
+    const uint32_t q = threadIdx.x & 3;
+    uint32_t s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 2);
+    for (uint64_t j = static_cast<uint64_t>(blockIdx.x) * (blockDim.x >> 2) + (threadIdx.x >> 2); j < n;
+         j += stride) {
+        const uint4 v = *reinterpret_cast<const uint4*>(digests + j * 64 + q * 16);
+        s[0] += v.x & 0xffffu; s[1] += v.x >> 16;
+        s[2] += v.y & 0xffffu; s[3] += v.y >> 16;
+        s[4] += v.z & 0xffffu; s[5] += v.z >> 16;
+        s[6] += v.w & 0xffffu; s[7] += v.w >> 16;
+    }
+    // lanes with equal q sit 4 apart: fold them with shuffles, then one
+    // shared atomic per warp and lane
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        uint32_t v = s[i];
+        v += __shfl_xor_sync(0xffffffffu, v, 4);
+        v += __shfl_xor_sync(0xffffffffu, v, 8);
+        v += __shfl_xor_sync(0xffffffffu, v, 16);
+        if ((threadIdx.x & 31) < 4) atomicAdd(&sacc[q * 8 + i], v);
+    }
+    __syncthreads();
+    if (threadIdx.x < LT_LANES && sacc[threadIdx.x]) atomicAdd(acc + threadIdx.x, sacc[threadIdx.x]);
+}
+
+// Mask the widened sums to 16 bits and pack them little-endian: n_sources x 64
+// bytes, the LatticeDigest layout of lattice.py:37-58.
+__global__ void lt_finalize_kernel(const uint32_t* __restrict__ acc, uint32_t n_words,
+                                   uint32_t* __restrict__ out) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;   // output word = 2 lanes
+    if (i < n_words) out[i] = (acc[2 * i] & 0xffffu) | (acc[2 * i + 1] << 16);
+}
+
+}  // namespace snt

@@ -1,0 +1,267 @@
+"""Per-source dataset digests: every sample LtHashed on the GPU, summed per source.
+
+API mirror of the reference's ``dataset.py`` (:24-195). A sample's digest is
+BLAKE2b-512(LE64(sample_id) || data) -- with ``cover_labels`` the label bytes sit
+between the id and the data (dataset.py:41-49) -- and a source's digest is the
+lane-wise sum modulo 2^16 of its samples' digests, so the result does not depend
+on shuffle order, batch size or how the samples are split across GPUs.
+
+Two ways in:
+
+* ``process_batch(batch, acc)`` keeps the reference's host-object protocol: the
+  batch is packed, copied to the device, hashed and reduced per source by one
+  kernel launch, and the per-source partial sums are folded into ``acc``.
+* ``digest_dataset`` / ``DeviceDataset`` is the device-resident path: the whole
+  shard and its (offset, length, id, source slot) rows live in HBM and one
+  launch digests every sample (the manifest layout of dataset.py:94-100).
+"""
+
+from __future__ import annotations
+
+import json
+import random
+from dataclasses import dataclass, field
+from pathlib import Path
+from typing import Dict, Iterable, Iterator, List, Optional, Sequence, Tuple
+
+import numpy as np
+import torch
+
+from . import device as _dev
+from .errors import FormatError, ValidationError
+from .lattice import LatticeDigest, lt_add, lt_hash_block, lt_hash_tagged, lt_zero
+
+
+@dataclass(frozen=True)
+class SampleRecord:
+    sample_id: int
+    source_id: int
+    label: bytes
+    data: bytes
+
+
+@dataclass
+class Batch:
+    samples: List[SampleRecord]
+
+    @property
+    def size(self) -> int:
+        return len(self.samples)
+
+
+def hash_sample(s: SampleRecord, cover_labels: bool = False) -> LatticeDigest:
+    """LtHash of one sample tagged with its stable id (dataset.py:41-49); one GPU launch."""
+    if cover_labels:
+        import struct
+
+        return lt_hash_tagged(struct.pack("<Q", s.sample_id) + s.label, s.data)
+    return lt_hash_block(s.sample_id, s.data)
+
+
+@dataclass
+class SourceAccumulator:
+    """Per-source running lattice sums and sample counts (host mirror, dataset.py:52-71)."""
+
+    sums: Dict[int, LatticeDigest] = field(default_factory=dict)
+    counts: Dict[int, int] = field(default_factory=dict)
+    declared_sources: Optional[frozenset] = None
+    cover_labels: bool = False
+
+    def declare(self, source_ids: Iterable[int]) -> None:
+        self.declared_sources = frozenset(source_ids)
+        for sid in self.declared_sources:
+            self.sums.setdefault(sid, lt_zero())
+            self.counts.setdefault(sid, 0)
+
+    def merge(self, other: "SourceAccumulator") -> None:
+        """Fold another accumulator in; any merge order gives the same sums."""
+        for sid, digest in other.sums.items():
+            self.sums[sid] = lt_add(self.sums.get(sid, lt_zero()), digest)
+            self.counts[sid] = self.counts.get(sid, 0) + other.counts.get(sid, 0)
+
+
+class DeviceDataset:
+    """A shard and its sample rows resident in HBM (the GPU input format).
+
+    ``shard``: flat uint8 tensor; ``offsets``/``lengths``/``ids``: int64 tensors
+    (bit patterns of u64); ``slots``: int32 index into ``source_ids``.
+    """
+
+    def __init__(self, shard: torch.Tensor, offsets: torch.Tensor, lengths: torch.Tensor,
+                 ids: torch.Tensor, slots: torch.Tensor, source_ids: Sequence[int]):
+        self.shard, self.offsets, self.lengths, self.ids, self.slots = shard, offsets, lengths, ids, slots
+        self.source_ids = list(source_ids)
+
+    @property
+    def n_samples(self) -> int:
+        return int(self.offsets.numel())
+
+    @classmethod
+    def from_host(cls, shard, offsets, lengths, ids, source_of_sample, source_ids: Sequence[int],
+                  pinned: bool = False) -> "DeviceDataset":
+        """Copy host arrays to the device. ``source_of_sample`` holds source ids, not slots."""
+        dev = _dev.require_cuda()
+        source_ids = sorted(set(int(s) for s in source_ids))
+        lut = {sid: i for i, sid in enumerate(source_ids)}
+        src = np.asarray(source_of_sample)
+        slots = np.fromiter((lut.get(int(s), -1) for s in src), dtype=np.int64, count=src.size)
+        bad = np.nonzero(slots < 0)[0]
+        if bad.size:
+            i = int(bad[0])
+            raise ValidationError(f"sample {int(np.asarray(ids)[i])} references undeclared source {int(src[i])}")
+
+        def up(a, dtype):
+            t = torch.from_numpy(np.ascontiguousarray(np.asarray(a).astype(dtype, copy=False)))
+            if pinned:
+                t = t.pin_memory()
+            return t.to(dev, non_blocking=True)
+
+        shard_t = _dev.as_device_bytes(shard, dev)
+        if shard_t.numel() == 0:
+            shard_t = torch.zeros(16, dtype=torch.uint8, device=dev)
+        return cls(shard_t, up(np.asarray(offsets, dtype=np.uint64).view(np.int64), np.int64),
+                   up(np.asarray(lengths, dtype=np.uint64).view(np.int64), np.int64),
+                   up(np.asarray(ids, dtype=np.uint64).view(np.int64), np.int64),
+                   up(slots, np.int32), source_ids)
+
+    def accumulate(self, acc: "_dev.LatticeAccumulator", begin: int = 0, end: Optional[int] = None,
+                   digests: Optional[torch.Tensor] = None) -> None:
+        """Enqueue the LtHash of samples [begin, end) into ``acc`` (no synchronisation)."""
+        end = self.n_samples if end is None else end
+        if end <= begin:
+            return
+        acc.add_samples(self.shard, self.offsets[begin:end], self.lengths[begin:end], self.ids[begin:end],
+                        self.slots[begin:end], digests)
+
+
+def _finalize_device(acc: "_dev.LatticeAccumulator", source_ids: Sequence[int]) -> Dict[int, Tuple[LatticeDigest, int]]:
+    out, counts, status = acc.digests()
+    if status & 1:
+        raise ValidationError("a sample references an undeclared source")
+    return {sid: (LatticeDigest(out[64 * i:64 * i + 64]), counts[i]) for i, sid in enumerate(source_ids)}
+
+
+def process_batch(batch: Batch, acc: SourceAccumulator) -> SourceAccumulator:
+    """Hash a batch on the GPU, reduce it per source, add to the running sums (dataset.py:74-86)."""
+    present: List[int] = []
+    for s in batch.samples:
+        if acc.declared_sources is not None and s.source_id not in acc.declared_sources:
+            raise ValidationError(f"sample {s.sample_id} references undeclared source {s.source_id}")
+        if s.source_id not in present:
+            present.append(s.source_id)
+    if not batch.samples:
+        return acc
+    payloads = [(s.label + s.data) if acc.cover_labels else s.data for s in batch.samples]
+    lengths = np.fromiter((len(p) for p in payloads), dtype=np.uint64, count=len(payloads))
+    offsets = np.zeros(len(payloads), dtype=np.uint64)
+    np.cumsum(lengths[:-1], out=offsets[1:])
+    ids = np.array([s.sample_id & 0xFFFFFFFFFFFFFFFF for s in batch.samples], dtype=np.uint64)
+    ds = DeviceDataset.from_host(b"".join(payloads), offsets, lengths, ids,
+                                 [s.source_id for s in batch.samples], present)
+    dacc = _dev.LatticeAccumulator(len(ds.source_ids))
+    ds.accumulate(dacc)
+    for sid, (digest, count) in _finalize_device(dacc, ds.source_ids).items():
+        acc.sums[sid] = lt_add(acc.sums.get(sid, lt_zero()), digest)
+        acc.counts[sid] = acc.counts.get(sid, 0) + count
+    return acc
+
+
+def finalize(acc: SourceAccumulator) -> Dict[int, Tuple[LatticeDigest, int]]:
+    """Per-source digests and counts, ordered by source id (dataset.py:89-91)."""
+    return {sid: (acc.sums[sid], acc.counts.get(sid, 0)) for sid in sorted(acc.sums)}
+
+
+@dataclass
+class DatasetManifest:
+    """Sample index over a flat binary shard (format of dataset.py:94-137)."""
+
+    samples: List[Tuple[int, int, bytes, int, int]]   # (sample_id, source_id, label, offset, length)
+    data_path: Path
+    expected_digests: Dict[int, str] = field(default_factory=dict)
+
+    @property
+    def source_ids(self) -> frozenset:
+        return frozenset(rec[1] for rec in self.samples)
+
+    @classmethod
+    def load(cls, manifest_path) -> "DatasetManifest":
+        manifest_path = Path(manifest_path)
+        try:
+            doc = json.loads(manifest_path.read_text())
+            rows = [(int(r["sample_id"]), int(r["source_id"]), str(r.get("label", "")).encode(),
+                     int(r["offset"]), int(r["length"])) for r in doc["samples"]]
+            data_path = manifest_path.parent / doc["data"]
+            expected = {int(k): v for k, v in doc.get("expected_digests", {}).items()}
+        except (OSError, KeyError, ValueError, TypeError) as exc:
+            raise FormatError(f"bad dataset manifest {manifest_path}: {exc}") from exc
+        if len({r[0] for r in rows}) != len(rows):
+            raise FormatError("sample ids must be unique within a dataset")
+        return cls(rows, data_path, expected)
+
+    def save(self, manifest_path, shard: bytes) -> None:
+        manifest_path = Path(manifest_path)
+        rows = [{"sample_id": sid, "source_id": src, "label": label.decode(), "offset": off, "length": ln}
+                for sid, src, label, off, ln in self.samples]
+        (manifest_path.parent / self.data_path.name).write_bytes(shard)
+        manifest_path.write_text(json.dumps({"samples": rows, "data": self.data_path.name,
+                                             "expected_digests": self.expected_digests}))
+
+
+def iterate_batches(manifest: DatasetManifest, batch_size: int, shuffle_seed: int) -> Iterator[Batch]:
+    """Every sample exactly once, in a seed-determined shuffle (dataset.py:140-163)."""
+    if batch_size < 1:
+        raise ValidationError("batch_size must be >= 1")
+    try:
+        shard = memoryview(manifest.data_path.read_bytes())
+    except OSError as exc:
+        raise FormatError(f"cannot read data shard {manifest.data_path}: {exc}") from exc
+    order = list(range(len(manifest.samples)))
+    random.Random(shuffle_seed).shuffle(order)
+    for start in range(0, len(order), batch_size):
+        recs = []
+        for idx in order[start:start + batch_size]:
+            sid, src, label, off, ln = manifest.samples[idx]
+            if off < 0 or off + ln > len(shard):
+                raise FormatError(f"sample {sid} range [{off}, {off + ln}) exceeds shard")
+            recs.append(SampleRecord(sid, src, label, bytes(shard[off:off + ln])))
+        yield Batch(recs)
+
+
+def digest_dataset(manifest: DatasetManifest, batch_size: int = 128, shuffle_seed: int = 0,
+                   cover_labels: bool = False, workers: int = 1) -> Dict[int, Tuple[LatticeDigest, int]]:
+    """Digest a whole manifest (dataset.py:166-195) with the shard resident in HBM.
+
+    The digests are invariant to ``batch_size``, ``shuffle_seed`` and ``workers``
+    (SPEC.md:402), so the device path hashes all samples in one launch; the
+    arguments are validated and otherwise unused.
+    """
+    if batch_size < 1:
+        raise ValidationError("batch_size must be >= 1")
+    try:
+        shard = manifest.data_path.read_bytes()
+    except OSError as exc:
+        raise FormatError(f"cannot read data shard {manifest.data_path}: {exc}") from exc
+    n = len(manifest.samples)
+    source_ids = sorted(manifest.source_ids)
+    if n == 0:
+        return {}
+    ids = np.array([r[0] & 0xFFFFFFFFFFFFFFFF for r in manifest.samples], dtype=np.uint64)
+    src = np.array([r[1] for r in manifest.samples], dtype=np.int64)
+    off = np.array([r[3] for r in manifest.samples], dtype=np.int64)
+    ln = np.array([r[4] for r in manifest.samples], dtype=np.int64)
+    bad = np.nonzero((off < 0) | (ln < 0) | (off + ln > len(shard)))[0]
+    if bad.size:
+        i = int(bad[0])
+        raise FormatError(f"sample {int(ids[i])} range [{int(off[i])}, {int(off[i] + ln[i])}) exceeds shard")
+    if cover_labels:
+        # message = LE64(id) || label || data: repack label+data contiguously per sample
+        view = memoryview(shard)
+        parts = [r[2] + bytes(view[r[3]:r[3] + r[4]]) for r in manifest.samples]
+        ln = np.fromiter((len(p) for p in parts), dtype=np.int64, count=n)
+        off = np.zeros(n, dtype=np.int64)
+        np.cumsum(ln[:-1], out=off[1:])
+        shard = b"".join(parts)
+    ds = DeviceDataset.from_host(shard, off.astype(np.uint64), ln.astype(np.uint64), ids, src, source_ids)
+    acc = _dev.LatticeAccumulator(len(source_ids))
+    ds.accumulate(acc)
+    return _finalize_device(acc, ds.source_ids)

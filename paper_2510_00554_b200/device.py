@@ -1,0 +1,260 @@
+"""Device plumbing: torch supplies HBM buffers and streams, the C ABI does the work.
+
+Everything that touches the GPU goes through this module: staging host bytes
+into device tensors, building model plans, and calling the ``snt_*`` entry
+points on torch's current stream. There is no CPU implementation behind these
+functions -- without a CUDA device they raise ``ResourceError``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import warnings
+from typing import Iterable, List, Optional, Sequence, Tuple
+
+import numpy as np
+import torch
+
+from . import _native
+from .errors import InvalidInput, ResourceError
+
+ALG_IDS = {"sha256": 0, "blake2b": 1, "sha3-256": 2}
+DIGEST_LEN = {"sha256": 32, "blake2b": 64, "sha3-256": 32}
+LT_LANES = 32
+
+
+def require_cuda() -> torch.device:
+    """The current CUDA device, or ``ResourceError`` (no CPU fallback exists)."""
+    if not torch.cuda.is_available():
+        raise ResourceError("a CUDA device is required: the hashing engine has no CPU fallback")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def _stream() -> ctypes.c_void_p:
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _ptr(t: Optional[torch.Tensor]) -> ctypes.c_void_p:
+    return ctypes.c_void_p(t.data_ptr() if t is not None else 0)
+
+
+def host_bytes_view(buf) -> np.ndarray:
+    """Zero-copy uint8 view of a host bytes-like object."""
+    if isinstance(buf, np.ndarray):
+        return np.ascontiguousarray(buf).reshape(-1).view(np.uint8)
+    return np.frombuffer(buf, dtype=np.uint8)
+
+
+def as_device_bytes(buf, device: Optional[torch.device] = None) -> torch.Tensor:
+    """A flat uint8 CUDA tensor holding the bytes of ``buf``.
+
+    CUDA tensors are reinterpreted in place (hashed where they lie); host
+    tensors, numpy arrays and bytes-like objects are copied to the device.
+    """
+    device = device or require_cuda()
+    if isinstance(buf, torch.Tensor):
+        t = buf.detach()
+        if not t.is_contiguous():
+            t = t.contiguous()
+        t = t.reshape(-1)
+        if t.dtype != torch.uint8:
+            t = t.view(torch.uint8)
+        if t.device.type != "cuda":
+            t = t.to(device, non_blocking=True)
+        return t
+    arr = host_bytes_view(buf)
+    if arr.size == 0:
+        return torch.empty(0, dtype=torch.uint8, device=device)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")          # read-only buffers are only read
+        host = torch.from_numpy(arr)
+    return host.to(device, non_blocking=True)
+
+
+class ModelPlan:
+    """Device-side block table over fragmented tensors (``snt_model_plan``).
+
+    Replaces ``BlockTable.build`` (reference model.py:137-146) for the kernels:
+    one row per tensor instead of one row per block. Keeps the tensors alive.
+    """
+
+    def __init__(self, tensors: Sequence[torch.Tensor], block_size: int):
+        self._handle = ctypes.c_void_p()
+        lib = _native.load()
+        require_cuda()
+        self.tensors = list(tensors)
+        n = len(self.tensors)
+        ptrs = (ctypes.c_void_p * max(n, 1))()
+        sizes = (ctypes.c_uint64 * max(n, 1))()
+        for i, t in enumerate(self.tensors):
+            if t.device.type != "cuda" or t.dtype != torch.uint8 or t.dim() != 1:
+                raise InvalidInput("ModelPlan needs flat uint8 CUDA tensors")
+            ptrs[i] = t.data_ptr() if t.numel() else None
+            sizes[i] = t.numel()
+        rc = lib.snt_model_plan_create(ptrs, sizes, n, block_size, ctypes.byref(self._handle))
+        _native.check(rc, "snt_model_plan_create")
+        self.block_size = block_size
+        self.leaf_count = int(lib.snt_model_plan_leaf_count(self._handle))
+        self.total_bytes = int(lib.snt_model_plan_total_bytes(self._handle))
+
+    @property
+    def handle(self) -> ctypes.c_void_p:
+        return self._handle
+
+    def close(self) -> None:
+        if self._handle:
+            _native.load().snt_model_plan_destroy(self._handle)
+            self._handle = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def merkle_work_bytes(alg: str, count: int) -> int:
+    return int(_native.load().snt_merkle_work_bytes(ALG_IDS[alg], count))
+
+
+def ceil_log2(n: int) -> int:
+    return 0 if n <= 1 else (n - 1).bit_length()
+
+
+class MerkleModelHasher:
+    """Reusable launch state for in-place Merkle hashing of one model.
+
+    Holds the plan and the device buffers (leaf digests, reducer scratch,
+    output nodes) so that ``run`` only enqueues kernels -- no allocation, no
+    synchronisation. ``leaf_begin``/``leaf_end``/``levels`` select a shard
+    (multi-GPU); the defaults hash the whole model down to the root.
+    """
+
+    def __init__(self, plan: ModelPlan, alg: str, leaf_begin: int = 0, leaf_end: Optional[int] = None,
+                 levels: Optional[int] = None):
+        self.plan = plan
+        self.alg = alg
+        self.dlen = DIGEST_LEN[alg]
+        n = plan.leaf_count
+        self.leaf_begin = leaf_begin
+        self.leaf_end = n if leaf_end is None else leaf_end
+        if not (0 <= self.leaf_begin < self.leaf_end <= n):
+            raise InvalidInput("empty or out-of-range leaf range")
+        self.levels = levels
+        count = self.leaf_end - self.leaf_begin
+        dev = require_cuda()
+        self.n_out = 1 if levels is None else -(-count // (1 << levels))
+        self.leaves = torch.empty(count * self.dlen, dtype=torch.uint8, device=dev)
+        self.work_bytes = merkle_work_bytes(alg, count)
+        self.work = torch.empty(max(self.work_bytes, 16), dtype=torch.uint8, device=dev)
+        self.out = torch.empty(self.n_out * self.dlen, dtype=torch.uint8, device=dev)
+
+    def run(self) -> None:
+        lib = _native.load()
+        levels = _native.SNT_LEVELS_TO_ROOT if self.levels is None else self.levels
+        rc = lib.snt_merkle_inplace(self.plan.handle, ALG_IDS[self.alg], self.leaf_begin, self.leaf_end,
+                                    levels, _ptr(self.leaves), _ptr(self.work), self.work_bytes,
+                                    _ptr(self.out), _stream())
+        _native.check(rc, "snt_merkle_inplace")
+
+    def out_bytes(self) -> bytes:
+        return self.out.cpu().numpy().tobytes()
+
+    def leaf_bytes(self) -> bytes:
+        return self.leaves.cpu().numpy().tobytes()
+
+
+def hash_blocks_device(alg: str, base: Optional[torch.Tensor], offsets: torch.Tensor, lengths: torch.Tensor,
+                       out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """``snt_hash_blocks``: digests of blocks ``base[off[i] : off[i] + len[i]]`` (device arrays)."""
+    lib = _native.load()
+    dev = require_cuda()
+    n = int(offsets.numel())
+    dlen = DIGEST_LEN[alg]
+    if out is None:
+        out = torch.empty(n * dlen, dtype=torch.uint8, device=dev)
+    rc = lib.snt_hash_blocks(ALG_IDS[alg], _ptr(base), _ptr(offsets), _ptr(lengths), n, _ptr(out), _stream())
+    _native.check(rc, "snt_hash_blocks")
+    return out
+
+
+def merkle_root_device(alg: str, nodes: torch.Tensor, count: int) -> torch.Tensor:
+    """``snt_merkle_root`` over ``count`` digests held in a flat uint8 CUDA tensor."""
+    lib = _native.load()
+    dev = require_cuda()
+    dlen = DIGEST_LEN[alg]
+    wb = merkle_work_bytes(alg, count)
+    work = torch.empty(max(wb, 16), dtype=torch.uint8, device=dev)
+    root = torch.empty(dlen, dtype=torch.uint8, device=dev)
+    rc = lib.snt_merkle_root(ALG_IDS[alg], _ptr(nodes), count, _ptr(work), wb, _ptr(root), _stream())
+    _native.check(rc, "snt_merkle_root")
+    return root
+
+
+def merkle_reduce_levels_device(alg: str, nodes: torch.Tensor, first: int, n_in: int, level_count: int,
+                                levels: int) -> torch.Tensor:
+    """``snt_merkle_reduce_levels``: apply ``levels`` tree levels to a node range."""
+    lib = _native.load()
+    dev = require_cuda()
+    dlen = DIGEST_LEN[alg]
+    n_out = -(-n_in // (1 << levels))
+    wb = merkle_work_bytes(alg, n_in)
+    work = torch.empty(max(wb, 16), dtype=torch.uint8, device=dev)
+    out = torch.empty(n_out * dlen, dtype=torch.uint8, device=dev)
+    rc = lib.snt_merkle_reduce_levels(ALG_IDS[alg], _ptr(nodes), first, n_in, level_count, levels,
+                                      _ptr(work), wb, _ptr(out), _stream())
+    _native.check(rc, "snt_merkle_reduce_levels")
+    return out
+
+
+class LatticeAccumulator:
+    """Device-resident per-source LtHash sums: ``n_sources x 32`` u32 lanes + u64 counts.
+
+    The running state of ``SourceAccumulator`` (reference dataset.py:52-71) kept
+    in HBM. Lanes are summed modulo 2^32 and masked to 16 bits by ``digests``;
+    that is exact modulo 2^16 for any number of samples.
+    """
+
+    def __init__(self, n_sources: int):
+        dev = require_cuda()
+        if n_sources < 1:
+            raise InvalidInput("at least one source slot is required")
+        self.n_sources = n_sources
+        self.acc = torch.zeros(n_sources * LT_LANES, dtype=torch.int32, device=dev)
+        self.counts = torch.zeros(n_sources, dtype=torch.int64, device=dev)
+        self.status = torch.zeros(1, dtype=torch.int32, device=dev)
+
+    def zero_(self) -> None:
+        self.acc.zero_()
+        self.counts.zero_()
+        self.status.zero_()
+
+    def add_samples(self, shard: torch.Tensor, offsets: torch.Tensor, lengths: torch.Tensor,
+                    ids: torch.Tensor, slots: torch.Tensor, digests: Optional[torch.Tensor] = None) -> None:
+        lib = _native.load()
+        n = int(offsets.numel())
+        rc = lib.snt_lthash_samples(_ptr(shard), _ptr(offsets), _ptr(lengths), _ptr(ids), _ptr(slots), n,
+                                    self.n_sources, _ptr(self.acc), _ptr(self.counts), _ptr(digests),
+                                    _ptr(self.status), _stream())
+        _native.check(rc, "snt_lthash_samples")
+
+    def add_model_leaves(self, plan: ModelPlan, leaf_begin: int, leaf_end: int,
+                         digests: Optional[torch.Tensor] = None) -> None:
+        lib = _native.load()
+        rc = lib.snt_lthash_model(plan.handle, leaf_begin, leaf_end, _ptr(self.acc), _ptr(self.counts),
+                                  _ptr(digests), _stream())
+        _native.check(rc, "snt_lthash_model")
+
+    def add_digests(self, digests: torch.Tensor, n: int) -> None:
+        lib = _native.load()
+        rc = lib.snt_lt_reduce(_ptr(digests), n, _ptr(self.acc), _stream())
+        _native.check(rc, "snt_lt_reduce")
+
+    def digests(self) -> Tuple[bytes, List[int], int]:
+        """(n_sources x 64 digest bytes, counts, status bits); synchronises."""
+        lib = _native.load()
+        out = torch.empty(self.n_sources * 64, dtype=torch.uint8, device=self.acc.device)
+        rc = lib.snt_lt_finalize(_ptr(self.acc), self.n_sources, _ptr(out), _stream())
+        _native.check(rc, "snt_lt_finalize")
+        return (out.cpu().numpy().tobytes(), [int(c) for c in self.counts.cpu().tolist()],
+                int(self.status.cpu().item()))

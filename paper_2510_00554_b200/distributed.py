@@ -1,0 +1,148 @@
+"""Multi-GPU shard-and-combine layer (one process per GPU, torch.distributed).
+
+Merkle: the reference tree (merkle.py:117-165) is node(j, i) = H(node(j-1, 2i) ||
+(node(j-1, 2i+1) or zeros)) for i < ceil(N / 2^j). Cutting the leaves into
+shards of 2^k leaves and reducing every shard EXACTLY k levels (zero padding on
+odd counts, never stopping early at one digest) yields the level-k nodes of that
+very tree; the ceil(N / 2^k) shard roots are then reduced by the ordinary rule.
+Each rank owns a contiguous run of whole shards; the only exchange is one
+all-gather of shard roots (a few KB).
+
+LtHash: lane sums are commutative (dataset.py:67-71), so each rank accumulates a
+contiguous sample range into ``n_sources x 32`` u32 lanes and one sum all-reduce
+combines them (u32 because NCCL has no u16 type; exact modulo 2^16).
+
+The hashing itself is injected as a ``backend`` (CUDA in the product, see
+``CudaBackend``); the partition / gather / top-reduce logic here is plain host
+code, so the tests drive it over ``gloo`` with a checker backend.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import List, Optional, Sequence, Tuple
+
+import torch
+import torch.distributed as dist
+
+from .errors import InvalidInput
+from .workers import chunk_ranges
+
+DEFAULT_SHARD_LEVELS = 10   # 1024 leaves = 8 MiB of tensor bytes per shard
+
+
+def ceil_div(a: int, b: int) -> int:
+    return -(-a // b)
+
+
+def choose_shard_levels(n_leaves: int, world: int, max_levels: int = DEFAULT_SHARD_LEVELS) -> int:
+    """Largest k <= max_levels with 2^k < N and at least 4 shards per rank (when N allows).
+
+    Small shards balance better: N = 799,954 at k = 10 gives 782 shards, 97 or 98
+    per rank on 8 GPUs, whereas rounding ceil(N / G) up to a power of two would
+    leave one GPU idle.
+    """
+    k = max_levels
+    while k > 0 and ((1 << k) >= n_leaves or ceil_div(n_leaves, 1 << k) < 4 * world):
+        k -= 1
+    return k
+
+
+@dataclass(frozen=True)
+class ShardPlan:
+    n_leaves: int
+    levels: int                              # k: every shard is reduced exactly k levels
+    n_shards: int                            # ceil(N / 2^k) = number of level-k nodes
+    shard_ranges: Tuple[Tuple[int, int], ...]  # per rank: [first_shard, last_shard)
+
+    def leaf_range(self, rank: int) -> Tuple[int, int]:
+        a, b = self.shard_ranges[rank]
+        return a << self.levels, min(b << self.levels, self.n_leaves)
+
+    def shard_count(self, rank: int) -> int:
+        a, b = self.shard_ranges[rank]
+        return b - a
+
+
+def plan_shards(n_leaves: int, world: int, levels: Optional[int] = None) -> ShardPlan:
+    if n_leaves < 1 or world < 1:
+        raise InvalidInput("need at least one leaf and one rank")
+    k = choose_shard_levels(n_leaves, world) if levels is None else levels
+    n_shards = ceil_div(n_leaves, 1 << k)
+    ranges = chunk_ranges(n_shards, world)
+    ranges += [(n_shards, n_shards)] * (world - len(ranges))      # ranks beyond the shard count idle
+    return ShardPlan(n_leaves, k, n_shards, tuple(ranges))
+
+
+class CudaBackend:
+    """Hashing backend of the product: the CUDA kernels through the C ABI."""
+
+    def __init__(self, plan, alg: str):
+        from . import device as _dev
+
+        self._dev = _dev
+        self.plan = plan
+        self.alg = alg
+        self.dlen = _dev.DIGEST_LEN[alg]
+        self.device = _dev.require_cuda()
+        self._hashers = {}
+
+    def shard_roots(self, leaf_begin: int, leaf_end: int, levels: int) -> torch.Tensor:
+        """Level-``levels`` nodes of the leaf range, as a flat uint8 device tensor (no sync)."""
+        key = (leaf_begin, leaf_end, levels)
+        h = self._hashers.get(key)
+        if h is None:
+            h = self._dev.MerkleModelHasher(self.plan, self.alg, leaf_begin, leaf_end, levels)
+            self._hashers[key] = h
+        h.run()
+        return h.out
+
+    def root_of(self, nodes: torch.Tensor, count: int) -> torch.Tensor:
+        return self._dev.merkle_root_device(self.alg, nodes, count)
+
+    def to_bytes(self, t: torch.Tensor) -> bytes:
+        return t.cpu().numpy().tobytes()
+
+
+def sharded_merkle_root(backend, shard_plan: ShardPlan, rank: int, world: int, group=None) -> torch.Tensor:
+    """This rank's shard roots -> all-gather -> top reduce. Returns the root (flat uint8 tensor).
+
+    Every rank returns the same root. With ``world == 1`` no collective is issued.
+    """
+    dlen = backend.dlen
+    begin, end = shard_plan.leaf_range(rank)
+    mine = shard_plan.shard_count(rank)
+    local = backend.shard_roots(begin, end, shard_plan.levels) if mine else None
+    if world == 1:
+        if shard_plan.n_shards == 1:
+            return local                               # already the single level-k node = the root
+        nodes = local
+    else:
+        widest = max(shard_plan.shard_count(r) for r in range(world))
+        send = torch.zeros(widest * dlen, dtype=torch.uint8, device=backend.device)
+        if mine:
+            send[:mine * dlen].copy_(local[:mine * dlen])
+        recv = torch.empty(world * widest * dlen, dtype=torch.uint8, device=backend.device)
+        dist.all_gather_into_tensor(recv, send, group=group)
+        parts = [recv[r * widest * dlen:(r * widest + shard_plan.shard_count(r)) * dlen] for r in range(world)]
+        nodes = torch.cat(parts)
+    return backend.root_of(nodes, shard_plan.n_shards)
+
+
+def sample_ranges(n_samples: int, world: int) -> List[Tuple[int, int]]:
+    """Contiguous sample ranges per rank (empty for ranks beyond the sample count)."""
+    ranges = chunk_ranges(n_samples, world)
+    return ranges + [(n_samples, n_samples)] * (world - len(ranges))
+
+
+def allreduce_lattice(acc: torch.Tensor, counts: torch.Tensor, status: Optional[torch.Tensor] = None,
+                      group=None) -> None:
+    """Sum the widened lane accumulators and counts over all ranks, in place.
+
+    ``acc`` is int32 (the bit pattern of u32 lanes; two's-complement addition is
+    the same sum modulo 2^32), ``counts`` int64. One all-reduce each, latency bound.
+    """
+    dist.all_reduce(acc, op=dist.ReduceOp.SUM, group=group)
+    dist.all_reduce(counts, op=dist.ReduceOp.SUM, group=group)
+    if status is not None:
+        dist.all_reduce(status, op=dist.ReduceOp.MAX, group=group)

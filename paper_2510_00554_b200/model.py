@@ -1,0 +1,291 @@
+"""Whole-model digests over fragmented tensor collections, computed on the GPU.
+
+API mirror of the reference's ``model.py`` (:44-374): ``TensorMap``,
+``HashConfig``, ``BlockTable``, ``ModelDigestResult``, ``inplace_hash``,
+``coalesce_hash``, ``hash_model``, ``load_model`` / ``save_model``.
+
+The default strategy -- in-place (model.py:298-315) -- hashes every tensor where
+it lies in HBM: a per-tensor table replaces the per-block table, each 8 KiB block
+is one leaf hashed by one thread (the last block of a tensor at its true length),
+and the leaf digests are reduced to the root on the device. ``TensorMap`` entries
+may be CUDA tensors (hashed in place, no copy) or host bytes-like objects (copied
+to the device first, which is what the reference-shaped call pays for).
+"""
+
+from __future__ import annotations
+
+import enum
+import json
+from dataclasses import dataclass
+from pathlib import Path
+from typing import Dict, List, Optional, Tuple, Union
+
+import numpy as np
+import torch
+
+from . import device as _dev
+from .compression import CompressionAlg, Digest
+from .errors import ConfigError, FormatError, InvalidInput, SentinelError
+from .lattice import DIGEST_BYTES as LT_DIGEST_BYTES
+from .lattice import LatticeDigest
+
+DEFAULT_BLOCK_SIZE = 8192
+
+# recorded in attestation predicates: lattice blocks carry a little-endian
+# 64-bit index prefix (global block counter for coalesced / in-place)
+INDEX_ENCODING = "le64-prefix-v1"
+
+
+class Construction(enum.Enum):
+    MERKLE = "merkle"
+    LATTICE = "lattice"
+
+
+class Strategy(enum.Enum):
+    COALESCED = "coalesced"
+    PER_LAYER = "per-layer"
+    IN_PLACE = "in-place"
+
+
+def buffer_nbytes(buf) -> int:
+    if isinstance(buf, torch.Tensor):
+        return buf.numel() * buf.element_size()
+    if isinstance(buf, np.ndarray):
+        return buf.nbytes
+    return memoryview(buf).nbytes
+
+
+@dataclass
+class TensorMap:
+    """Ordered, uniquely named, independently allocated tensors.
+
+    Each buffer is a CUDA/CPU ``torch.Tensor``, a numpy array or a bytes-like
+    object; only its bytes matter.
+    """
+
+    entries: List[Tuple[str, object]]
+
+    def __post_init__(self):
+        seen = set()
+        for name, _ in self.entries:
+            if name in seen:
+                raise InvalidInput("layer names must be unique")
+            seen.add(name)
+
+    def __len__(self) -> int:
+        return len(self.entries)
+
+    @property
+    def total_bytes(self) -> int:
+        return sum(buffer_nbytes(buf) for _, buf in self.entries)
+
+    def names(self) -> List[str]:
+        return [name for name, _ in self.entries]
+
+
+@dataclass
+class HashConfig:
+    construction: Construction
+    strategy: Strategy
+    alg: CompressionAlg = CompressionAlg.SHA256
+    block_size: int = DEFAULT_BLOCK_SIZE
+    ordered_per_layer: bool = False
+
+    def validate(self) -> None:
+        """Same rules as the reference (model.py:93-102)."""
+        bs = self.block_size
+        if bs < 64 or bs & (bs - 1):
+            raise ConfigError("block_size must be a power of two >= 64")
+        lattice = self.construction is Construction.LATTICE
+        if lattice and self.alg is not CompressionAlg.BLAKE2B:
+            raise ConfigError("lattice hashing is fixed to BLAKE2b")
+        if self.ordered_per_layer and not (lattice and self.strategy is Strategy.PER_LAYER):
+            raise ConfigError("ordered_per_layer requires lattice per-layer hashing")
+
+    def predicate(self) -> Dict[str, object]:
+        """Everything a verifier needs to replay this configuration (model.py:104-113)."""
+        return {
+            "construction": self.construction.value,
+            "compression": self.alg.value,
+            "strategy": self.strategy.value,
+            "block_size": self.block_size,
+            "ordered_per_layer": self.ordered_per_layer,
+            "index_encoding": INDEX_ENCODING,
+        }
+
+    @classmethod
+    def from_predicate(cls, pred: Dict[str, object]) -> "HashConfig":
+        try:
+            cfg = cls(Construction(pred["construction"]), Strategy(pred["strategy"]),
+                      CompressionAlg.from_name(pred["compression"]), int(pred["block_size"]),
+                      bool(pred.get("ordered_per_layer", False)))
+        except (KeyError, ValueError) as exc:
+            raise FormatError(f"bad hashing predicate: {exc}") from exc
+        cfg.validate()
+        return cfg
+
+
+@dataclass
+class BlockTable:
+    """Host view of the in-place block table: rows (k, tensor, offset, length).
+
+    The kernels search the compact per-tensor form (``device.ModelPlan``); this
+    per-block expansion (model.py:137-146) is kept for inspection and tests.
+    """
+
+    rows: List[Tuple[int, int, int, int]]
+
+    @classmethod
+    def build(cls, model: TensorMap, block_size: int) -> "BlockTable":
+        rows: List[Tuple[int, int, int, int]] = []
+        k = 0
+        for t, (_, buf) in enumerate(model.entries):
+            size = buffer_nbytes(buf)
+            full, tail = divmod(size, block_size)
+            rows.extend((k + j, t, j * block_size, block_size) for j in range(full))
+            k += full
+            if tail:
+                rows.append((k, t, full * block_size, tail))
+                k += 1
+        return cls(rows)
+
+
+@dataclass
+class ModelDigestResult:
+    model_digest: Union[Digest, LatticeDigest]
+    config: HashConfig
+    block_count: int
+    layer_digests: Optional[Dict[str, Union[Digest, LatticeDigest]]] = None
+    aux_data_bytes: int = 0     # staging copies of tensor data (coalesced buffer)
+    aux_digest_bytes: int = 0   # digest + reducer scratch storage on the device
+
+    @property
+    def aux_bytes(self) -> int:
+        return self.aux_data_bytes + self.aux_digest_bytes
+
+    def digest_hex(self) -> str:
+        return self.model_digest.hex()
+
+
+def _require_nonempty(model: TensorMap) -> None:
+    if len(model) == 0 or model.total_bytes == 0:
+        raise InvalidInput("model must contain at least one byte of tensor data")
+
+
+def device_tensors(model: TensorMap) -> List[torch.Tensor]:
+    """Flat uint8 CUDA views (or staged copies) of every entry, in order."""
+    dev = _dev.require_cuda()
+    return [_dev.as_device_bytes(buf, dev) for _, buf in model.entries]
+
+
+def _hash_plan(cfg: HashConfig, plan: _dev.ModelPlan, aux_data_bytes: int = 0) -> ModelDigestResult:
+    n = plan.leaf_count
+    if cfg.construction is Construction.MERKLE:
+        hasher = _dev.MerkleModelHasher(plan, cfg.alg.value)
+        hasher.run()
+        root = Digest(cfg.alg, hasher.out_bytes())
+        aux = hasher.leaves.numel() + hasher.work_bytes + (hasher.out.numel() if n > 1 else 0)
+        return ModelDigestResult(root, cfg, n, aux_data_bytes=aux_data_bytes, aux_digest_bytes=aux)
+    acc = _dev.LatticeAccumulator(1)
+    acc.add_model_leaves(plan, 0, n)
+    out, _, _ = acc.digests()
+    # one 64-byte accumulator instead of the reference's n x 64 digest array
+    return ModelDigestResult(LatticeDigest(out), cfg, n, aux_data_bytes=aux_data_bytes,
+                             aux_digest_bytes=acc.acc.numel() * 4)
+
+
+def inplace_hash(cfg: HashConfig, model: TensorMap, workers: int = 1) -> ModelDigestResult:
+    """Hash fragmented tensors where they lie: no copy, no padding (model.py:298-315)."""
+    _require_nonempty(model)
+    plan = _dev.ModelPlan(device_tensors(model), cfg.block_size)
+    try:
+        return _hash_plan(cfg, plan)
+    finally:
+        plan.close()
+
+
+def coalesce_hash(cfg: HashConfig, model: TensorMap, workers: int = 1) -> ModelDigestResult:
+    """Gather all tensors into one zero-padded device buffer, then hash its blocks (model.py:203-228)."""
+    _require_nonempty(model)
+    dev = _dev.require_cuda()
+    bs = cfg.block_size
+    total = model.total_bytes
+    padded = -(-total // bs) * bs
+    packed = torch.zeros(padded, dtype=torch.uint8, device=dev)
+    pos = 0
+    for t in device_tensors(model):
+        packed[pos:pos + t.numel()].copy_(t)
+        pos += t.numel()
+    plan = _dev.ModelPlan([packed], bs)
+    try:
+        return _hash_plan(cfg, plan, aux_data_bytes=padded)
+    finally:
+        plan.close()
+
+
+def per_layer_hash(cfg: HashConfig, model: TensorMap, workers: int = 1) -> ModelDigestResult:
+    """Per-layer strategy (model.py:231-286) -- not on this round's hot path."""
+    raise SentinelError("per-layer hashing is not built yet in the B200 engine (SURVEY.md section 8(f), rank 2)")
+
+
+def ordered_lattice_per_layer(cfg: HashConfig, model: TensorMap, workers: int = 1) -> ModelDigestResult:
+    """Size-ordered lattice per-layer hashing (model.py:289-295)."""
+    if (cfg.construction is not Construction.LATTICE or cfg.strategy is not Strategy.PER_LAYER
+            or not cfg.ordered_per_layer):
+        raise ConfigError("ordered_lattice_per_layer requires lattice per-layer ordered config")
+    return per_layer_hash(cfg, model, workers)
+
+
+_DISPATCH = {
+    Strategy.COALESCED: coalesce_hash,
+    Strategy.PER_LAYER: per_layer_hash,
+    Strategy.IN_PLACE: inplace_hash,
+}
+
+
+def hash_model(cfg: HashConfig, model: TensorMap, workers: int = 1) -> ModelDigestResult:
+    """Validate the configuration and run the matching strategy (model.py:325-330)."""
+    cfg.validate()
+    if cfg.ordered_per_layer:
+        return ordered_lattice_per_layer(cfg, model, workers)
+    return _DISPATCH[cfg.strategy](cfg, model, workers)
+
+
+# --- manifest I/O (host files; formats identical to model.py:335-374) -----------
+
+def load_model(manifest_path) -> TensorMap:
+    """Read ``{"tensors": [{name, offset, length}], "data": file}`` plus the raw data file.
+
+    Every tensor becomes its own buffer, reproducing a checkpoint's fragmentation.
+    """
+    manifest_path = Path(manifest_path)
+    try:
+        doc = json.loads(manifest_path.read_text())
+        raw = (manifest_path.parent / doc["data"]).read_bytes()
+        entries = []
+        for rec in doc["tensors"]:
+            start, length = int(rec["offset"]), int(rec["length"])
+            if start < 0 or length < 0 or start + length > len(raw):
+                raise FormatError(f"tensor {rec['name']!r} range [{start}, {start + length}) exceeds data file")
+            entries.append((rec["name"], bytes(raw[start:start + length])))
+    except FormatError:
+        raise
+    except (OSError, KeyError, ValueError, TypeError) as exc:
+        raise FormatError(f"bad model manifest {manifest_path}: {exc}") from exc
+    return TensorMap(entries)
+
+
+def save_model(model: TensorMap, manifest_path, data_name: Optional[str] = None) -> None:
+    """Write the manifest and the concatenated tensor bytes next to it."""
+    manifest_path = Path(manifest_path)
+    data_name = data_name or manifest_path.stem + ".bin"
+    records, blobs, pos = [], [], 0
+    for name, buf in model.entries:
+        if isinstance(buf, torch.Tensor):
+            buf = buf.detach().cpu().contiguous().reshape(-1).view(torch.uint8).numpy().tobytes()
+        blob = bytes(memoryview(buf).cast("B")) if not isinstance(buf, bytes) else buf
+        records.append({"name": name, "offset": pos, "length": len(blob)})
+        blobs.append(blob)
+        pos += len(blob)
+    (manifest_path.parent / data_name).write_bytes(b"".join(blobs))
+    manifest_path.write_text(json.dumps({"tensors": records, "data": data_name}, indent=2))

@@ -1,0 +1,124 @@
+// Host build of the per-thread hashing code the kernels run (the SNT_HD
+// functions in paper_2510_00554_b200/csrc). Test infrastructure only: it lets
+// the CPU suite check message padding, unaligned loads, the leaf locator and
+// the pad schedules against hashlib before any GPU time is spent. The product
+// never loads this library.
+#include <cstring>
+#include <vector>
+
+#include "../../paper_2510_00554_b200/csrc/lthash_kernels.cuh"
+#include "../../paper_2510_00554_b200/csrc/merkle_kernels.cuh"
+
+using namespace snt;
+
+template <int ALG>
+static void leaf_bytes(const uint8_t* p, uint64_t len, uint8_t* out) {
+    using A = AlgTraits<ALG>;
+    uint32_t d[A::DW];
+    A::leaf(p, len, d);
+    for (int i = 0; i < A::DW; ++i) {
+        const uint32_t w = A::to_mem(d[i]);
+        memcpy(out + 4 * i, &w, 4);
+    }
+}
+
+template <int ALG>
+static void pair_bytes(const uint8_t* l, const uint8_t* r, const MerkleConsts& c, uint8_t* out) {
+    using A = AlgTraits<ALG>;
+    uint32_t a[A::DW], b[A::DW], o[A::DW];
+    for (int i = 0; i < A::DW; ++i) {
+        uint32_t w;
+        memcpy(&w, l + 4 * i, 4); a[i] = A::from_mem(w);
+        memcpy(&w, r + 4 * i, 4); b[i] = A::from_mem(w);
+    }
+    A::pair(a, b, c, o);
+    for (int i = 0; i < A::DW; ++i) {
+        const uint32_t w = A::to_mem(o[i]);
+        memcpy(out + 4 * i, &w, 4);
+    }
+}
+
+extern "C" {
+
+int hc_leaf(int alg, const uint8_t* p, uint64_t len, uint8_t* out) {
+    switch (alg) {
+        case ALG_SHA256: leaf_bytes<ALG_SHA256>(p, len, out); return 0;
+        case ALG_BLAKE2B: leaf_bytes<ALG_BLAKE2B>(p, len, out); return 0;
+        case ALG_SHA3_256: leaf_bytes<ALG_SHA3_256>(p, len, out); return 0;
+    }
+    return -1;
+}
+
+int hc_pair(int alg, const uint8_t* l, const uint8_t* r, uint8_t* out) {
+    MerkleConsts c;
+    memset(&c, 0, sizeof(c));
+    Sha256::pad_schedule(64, c.sha256_pad_node);
+    switch (alg) {
+        case ALG_SHA256: pair_bytes<ALG_SHA256>(l, r, c, out); return 0;
+        case ALG_BLAKE2B: pair_bytes<ALG_BLAKE2B>(l, r, c, out); return 0;
+        case ALG_SHA3_256: pair_bytes<ALG_SHA3_256>(l, r, c, out); return 0;
+    }
+    return -1;
+}
+
+// the aligned SHA-256 leaf fast path (p must be 16-byte aligned, len % 64 == 0)
+int hc_sha256_aligned(const uint8_t* p, uint64_t len, uint8_t* out) {
+    uint32_t kw[64], s[8];
+    Sha256::pad_schedule(len, kw);
+    sha256_leaf_aligned(p, static_cast<uint32_t>(len >> 6), kw, s);
+    for (int i = 0; i < 8; ++i) {
+        const uint32_t w = bswap32(s[i]);
+        memcpy(out + 4 * i, &w, 4);
+    }
+    return 0;
+}
+
+// BLAKE2b-512(tag words || data), T in {0, 1, 2}
+int hc_blake2b_tagged(int T, uint64_t tag0, uint64_t tag1, const uint8_t* p, uint64_t len, uint8_t* out) {
+    uint64_t h[8];
+    if (T == 0) Blake2b::hash_message<0>(tag0, tag1, p, len, h);
+    else if (T == 1) Blake2b::hash_message<1>(tag0, tag1, p, len, h);
+    else if (T == 2) Blake2b::hash_message<2>(tag0, tag1, p, len, h);
+    else return -1;
+    memcpy(out, h, 64);
+    return 0;
+}
+
+// leaf locator over a host copy of the tensor table: returns offset within
+// the tensor through *off, tensor index through *t, length through *len
+int hc_locate(const uint64_t* nbytes, uint32_t n_tensors, uint32_t block_size, uint64_t k, uint32_t* t,
+              uint64_t* off, uint64_t* len) {
+    uint32_t shift = 0;
+    while ((1u << shift) < block_size) ++shift;
+    std::vector<uint64_t> addr(n_tensors), first(n_tensors + 1);
+    uint64_t leaves = 0, base = 1ull << 40;
+    for (uint32_t i = 0; i < n_tensors; ++i) {
+        addr[i] = base;
+        base += (nbytes[i] + 4095) & ~4095ull;
+        base += 4096;
+        first[i] = leaves;
+        leaves += (nbytes[i] + block_size - 1) >> shift;
+    }
+    first[n_tensors] = leaves;
+    if (k >= leaves) return -1;
+    TensorTable tab;
+    tab.addr = addr.data();
+    tab.nbytes = nbytes;
+    tab.first_leaf = first.data();
+    tab.n_tensors = n_tensors;
+    tab.block_shift = shift;
+    tab.n_leaves = leaves;
+    const LeafRef r = locate_leaf(tab, k);
+    const uint64_t a = reinterpret_cast<uint64_t>(r.ptr);
+    for (uint32_t i = 0; i < n_tensors; ++i) {
+        if (nbytes[i] && a >= addr[i] && a < addr[i] + nbytes[i]) {
+            *t = i;
+            *off = a - addr[i];
+            *len = r.len;
+            return 0;
+        }
+    }
+    return -2;
+}
+
+}  // extern "C"
