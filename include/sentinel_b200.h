@@ -44,6 +44,8 @@ const char* snt_strerror(int status);
 /* Last CUDA error string seen by this thread's failing call (diagnostics). */
 const char* snt_last_cuda_error(void);
 uint32_t snt_abi_version(void);
+/* Diagnostic: kernels launched by this library in this process so far. */
+uint64_t snt_debug_launch_count(void);
 /* 32, 64, 32 -- or 0 for an unknown algorithm. */
 uint32_t snt_digest_len(int alg);
 
@@ -65,6 +67,12 @@ uint64_t snt_model_plan_total_bytes(const snt_model_plan* plan);
 /* Bytes of scratch snt_merkle_inplace / snt_merkle_root need for `count`
  * input digests of `alg`. */
 size_t snt_merkle_work_bytes(int alg, uint64_t count);
+
+/* Leaf stage alone: hash_blocks over the in-place block table (model.py:300-305,
+ * merkle.py:93-114). Leaf k of [leaf_begin, leaf_end) is written at
+ * d_leaves + (k - leaf_begin) * digest_len. */
+int snt_merkle_leaves(const snt_model_plan* plan, int alg, uint64_t leaf_begin, uint64_t leaf_end,
+                      void* d_leaves, snt_stream_t stream);
 
 /* inplace_hash, MERKLE construction (model.py:298-310): hash leaves
  * [leaf_begin, leaf_end) of the plan and reduce them `levels` tree levels.
@@ -90,7 +98,10 @@ int snt_hash_blocks(int alg, const void* d_base, const uint64_t* d_off, const ui
  * `level_count` nodes in the whole tree. first must be a multiple of
  * 2^levels; first + n_in must be level_count or a multiple of 2^levels.
  * Writes ceil(n_in / 2^levels) nodes. An odd level pairs its last node with
- * zero bytes; levels are never skipped. d_out must not alias d_in. */
+ * zero bytes; levels are never skipped (a lone node is paired with zeros: the
+ * shard rule), so the reference's "fewer than two digests" InvalidState
+ * (merkle.py:125-126) is raised by the Python reduce_level wrapper, not here.
+ * d_out must not alias d_in. */
 int snt_merkle_reduce_levels(int alg, const void* d_in, uint64_t first, uint64_t n_in,
                              uint64_t level_count, uint32_t levels, void* d_work,
                              size_t work_bytes, void* d_out, snt_stream_t stream);

@@ -24,6 +24,7 @@ SIGNATURES = {
     "snt_strerror": (c_char_p, [c_int]),
     "snt_last_cuda_error": (c_char_p, []),
     "snt_abi_version": (c_uint32, []),
+    "snt_debug_launch_count": (c_uint64, []),
     "snt_digest_len": (c_uint32, [c_int]),
     "snt_model_plan_create": (c_int, [POINTER(c_void_p), POINTER(c_uint64), c_uint32, c_uint32,
                                       POINTER(c_void_p)]),
@@ -31,6 +32,7 @@ SIGNATURES = {
     "snt_model_plan_leaf_count": (c_uint64, [c_void_p]),
     "snt_model_plan_total_bytes": (c_uint64, [c_void_p]),
     "snt_merkle_work_bytes": (c_size_t, [c_int, c_uint64]),
+    "snt_merkle_leaves": (c_int, [c_void_p, c_int, c_uint64, c_uint64, c_void_p, c_void_p]),
     "snt_merkle_inplace": (c_int, [c_void_p, c_int, c_uint64, c_uint64, c_uint32, c_void_p, c_void_p,
                                    c_size_t, c_void_p, c_void_p]),
     "snt_hash_blocks": (c_int, [c_int, c_void_p, c_void_p, c_void_p, c_uint64, c_void_p, c_void_p]),

@@ -3,6 +3,7 @@
 // level-reducer launches. No torch types, no allocation on the hashing path.
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdio>
 #include <cstring>
 #include <new>
@@ -17,6 +18,9 @@ using namespace snt;
 namespace {
 
 thread_local char g_cuda_err[256] = "";
+
+// diagnostic only: number of kernels this library has launched in this process
+std::atomic<uint64_t> g_launches{0};
 
 int cuda_fail(cudaError_t e, const char* where) {
     snprintf(g_cuda_err, sizeof(g_cuda_err), "%s: %s", where, cudaGetErrorString(e));
@@ -87,6 +91,8 @@ const char* snt_strerror(int status) {
 const char* snt_last_cuda_error(void) { return g_cuda_err; }
 
 uint32_t snt_abi_version(void) { return 1; }
+
+uint64_t snt_debug_launch_count(void) { return g_launches.load(); }
 
 uint32_t snt_digest_len(int alg) {
     switch (alg) {
@@ -165,6 +171,7 @@ int launch_reduce(const uint8_t* in, uint64_t first, uint64_t n_in, uint64_t lev
     merkle_reduce_kernel<ALG><<<static_cast<unsigned>(n_out), REDUCE_THREADS, 0, s>>>(
         in, first, n_in, level_count, levels, c, out);
     SNT_CUDA(cudaGetLastError());
+    ++g_launches;
     return SNT_OK;
 }
 
@@ -215,6 +222,7 @@ int launch_leaves(const snt_model_plan* plan, uint64_t begin, uint64_t end, uint
     merkle_leaf_kernel<ALG><<<static_cast<unsigned>(grid), LEAF_THREADS, 0, s>>>(
         plan->table(), plan->consts, begin, end, d_leaves);
     SNT_CUDA(cudaGetLastError());
+    ++g_launches;
     return SNT_OK;
 }
 
@@ -225,6 +233,7 @@ int launch_blocks(const uint8_t* base, const uint64_t* off, const uint64_t* len,
     if (grid > 0x7fffffffull) return SNT_ERR_INVALID_INPUT;
     hash_blocks_kernel<ALG><<<static_cast<unsigned>(grid), LEAF_THREADS, 0, s>>>(base, off, len, n, out);
     SNT_CUDA(cudaGetLastError());
+    ++g_launches;
     return SNT_OK;
 }
 
@@ -245,12 +254,27 @@ int launch_lthash(const Items& items, uint64_t n, uint32_t n_sources, uint32_t* 
             items, n, n_sources, d_acc, counts, dig, d_status);
     }
     SNT_CUDA(cudaGetLastError());
+    ++g_launches;
     return SNT_OK;
 }
 
 }  // namespace
 
 extern "C" {
+
+int snt_merkle_leaves(const snt_model_plan* plan, int alg, uint64_t leaf_begin, uint64_t leaf_end,
+                      void* d_leaves, snt_stream_t stream) {
+    if (!plan || !d_leaves) return SNT_ERR_INVALID_INPUT;
+    if (!valid_alg(alg)) return SNT_ERR_CONFIG;
+    if (leaf_begin >= leaf_end || leaf_end > plan->n_leaves) return SNT_ERR_INVALID_INPUT;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    uint8_t* leaves = static_cast<uint8_t*>(d_leaves);
+    switch (alg) {
+        case SNT_SHA256: return launch_leaves<ALG_SHA256>(plan, leaf_begin, leaf_end, leaves, s);
+        case SNT_BLAKE2B: return launch_leaves<ALG_BLAKE2B>(plan, leaf_begin, leaf_end, leaves, s);
+        default: return launch_leaves<ALG_SHA3_256>(plan, leaf_begin, leaf_end, leaves, s);
+    }
+}
 
 int snt_merkle_inplace(const snt_model_plan* plan, int alg, uint64_t leaf_begin, uint64_t leaf_end,
                        uint32_t levels, void* d_leaves, void* d_work, size_t work_bytes, void* d_out,
@@ -306,8 +330,6 @@ int snt_merkle_reduce_levels(int alg, const void* d_in, uint64_t first, uint64_t
                              snt_stream_t stream) {
     if (!valid_alg(alg)) return SNT_ERR_CONFIG;
     if (!d_in || !d_out || n_in == 0 || levels == 0 || levels > 63) return SNT_ERR_INVALID_INPUT;
-    if (level_count < 2 && levels == 1 && first == 0 && n_in == level_count)
-        return SNT_ERR_INVALID_STATE;                                                 // merkle.py:125-126
     const uint64_t mask = (1ull << levels) - 1;
     const uint64_t end = first + n_in;
     if ((first & mask) || end > level_count || ((end & mask) && end != level_count))
@@ -366,6 +388,7 @@ int snt_lt_reduce(const void* d_digests, uint64_t n, uint32_t* d_acc, snt_stream
     lt_reduce_kernel<<<static_cast<unsigned>(grid), 256, 0, static_cast<cudaStream_t>(stream)>>>(
         static_cast<const uint8_t*>(d_digests), n, d_acc);
     SNT_CUDA(cudaGetLastError());
+    ++g_launches;
     return SNT_OK;
 }
 
@@ -375,6 +398,7 @@ int snt_lt_finalize(const uint32_t* d_acc, uint32_t n_sources, void* d_out, snt_
     lt_finalize_kernel<<<(n_words + 255) / 256, 256, 0, static_cast<cudaStream_t>(stream)>>>(
         d_acc, n_words, static_cast<uint32_t*>(d_out));
     SNT_CUDA(cudaGetLastError());
+    ++g_launches;
     return SNT_OK;
 }
 

@@ -78,7 +78,10 @@ class ModelPlan:
     one row per tensor instead of one row per block. Keeps the tensors alive.
     """
 
-    def __init__(self, tensors: Sequence[torch.Tensor], block_size: int):
+    def __init__(self, tensors: Sequence[torch.Tensor], block_size: int,
+                 sizes_override: Optional[Sequence[int]] = None):
+        """``sizes_override[i]`` gives tensor i's true byte length when ``tensors[i]`` is only a
+        placeholder (a tensor this rank never reads because its leaves belong to other ranks)."""
         self._handle = ctypes.c_void_p()
         lib = _native.load()
         require_cuda()
@@ -89,8 +92,9 @@ class ModelPlan:
         for i, t in enumerate(self.tensors):
             if t.device.type != "cuda" or t.dtype != torch.uint8 or t.dim() != 1:
                 raise InvalidInput("ModelPlan needs flat uint8 CUDA tensors")
-            ptrs[i] = t.data_ptr() if t.numel() else None
-            sizes[i] = t.numel()
+            nbytes = t.numel() if sizes_override is None else int(sizes_override[i])
+            ptrs[i] = t.data_ptr() if nbytes else None
+            sizes[i] = nbytes
         rc = lib.snt_model_plan_create(ptrs, sizes, n, block_size, ctypes.byref(self._handle))
         _native.check(rc, "snt_model_plan_create")
         self.block_size = block_size
@@ -156,6 +160,13 @@ class MerkleModelHasher:
                                     levels, _ptr(self.leaves), _ptr(self.work), self.work_bytes,
                                     _ptr(self.out), _stream())
         _native.check(rc, "snt_merkle_inplace")
+
+    def run_leaves_only(self) -> None:
+        """The leaf stage alone (``snt_merkle_leaves``); used to time the dominant kernel."""
+        lib = _native.load()
+        rc = lib.snt_merkle_leaves(self.plan.handle, ALG_IDS[self.alg], self.leaf_begin, self.leaf_end,
+                                   _ptr(self.leaves), _stream())
+        _native.check(rc, "snt_merkle_leaves")
 
     def out_bytes(self) -> bytes:
         return self.out.cpu().numpy().tobytes()

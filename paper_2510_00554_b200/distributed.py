@@ -129,6 +129,61 @@ def sharded_merkle_root(backend, shard_plan: ShardPlan, rank: int, world: int, g
     return backend.root_of(nodes, shard_plan.n_shards)
 
 
+def _first_leaves(sizes: Sequence[int], block_size: int) -> List[int]:
+    first, k = [], 0
+    for s in sizes:
+        first.append(k)
+        k += ceil_div(s, block_size)
+    first.append(k)
+    return first
+
+
+def staged_bytes(model, block_size: int, leaf_begin: int, leaf_end: int) -> int:
+    """Bytes of the tensors that own at least one leaf of [leaf_begin, leaf_end)."""
+    from .model import buffer_nbytes
+
+    sizes = [buffer_nbytes(buf) for _, buf in model.entries]
+    first = _first_leaves(sizes, block_size)
+    return sum(s for i, s in enumerate(sizes) if first[i] < leaf_end and first[i + 1] > leaf_begin)
+
+
+def hash_model_sharded(cfg, model, rank: int, world: int, group=None):
+    """In-place Merkle hash of one model across ``world`` GPUs (public multi-GPU entry point).
+
+    Every rank passes the same ``TensorMap``; a rank copies to its GPU only the
+    tensors that own leaves of its shard run (tensors already on the GPU are used
+    in place), hashes them, and all ranks combine the shard roots into the same
+    root ``hash_model`` returns on one GPU.
+    """
+    from . import device as _dev
+    from .compression import Digest
+    from .model import Construction, ModelDigestResult, Strategy, _require_nonempty, buffer_nbytes
+
+    cfg.validate()
+    if cfg.construction is not Construction.MERKLE or cfg.strategy is not Strategy.IN_PLACE:
+        raise InvalidInput("hash_model_sharded covers the in-place Merkle configuration")
+    _require_nonempty(model)
+    dev = _dev.require_cuda()
+    bs = cfg.block_size
+    sizes = [buffer_nbytes(buf) for _, buf in model.entries]
+    first = _first_leaves(sizes, bs)
+    sp = plan_shards(first[-1], world)
+    a, b = sp.leaf_range(rank)
+    placeholder = torch.zeros(16, dtype=torch.uint8, device=dev)
+    staged = []
+    for i, (_, buf) in enumerate(model.entries):
+        mine = first[i] < b and first[i + 1] > a
+        on_gpu = isinstance(buf, torch.Tensor) and buf.device.type == "cuda"
+        staged.append(_dev.as_device_bytes(buf, dev) if (mine or on_gpu) else placeholder)
+    plan = _dev.ModelPlan(staged, bs, sizes_override=sizes)
+    try:
+        backend = CudaBackend(plan, cfg.alg.value)
+        root = sharded_merkle_root(backend, sp, rank, world, group)
+        return ModelDigestResult(Digest(cfg.alg, backend.to_bytes(root)), cfg, first[-1])
+    finally:
+        plan.close()
+
+
 def sample_ranges(n_samples: int, world: int) -> List[Tuple[int, int]]:
     """Contiguous sample ranges per rank (empty for ranks beyond the sample count)."""
     ranges = chunk_ranges(n_samples, world)

@@ -1,0 +1,399 @@
+"""GPU parity: the CUDA path (through the C ABI) against the golden vectors and the oracles.
+
+Every comparison is bit-exact. Sizes the oracle finishes in seconds are compared
+directly (including full-size GPT-2 small, 652 MB, against the multi-threaded C
+oracle); the multi-shard and leaf-range paths are additionally checked through
+size-independent properties (shard roots recombine to the whole-model root).
+"""
+
+import hashlib
+import struct
+
+import numpy as np
+import pytest
+
+import inputs
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+ALGS = ["sha256", "blake2b", "sha3-256"]
+
+
+@pytest.fixture(scope="module")
+def pkg():
+    import paper_2510_00554_b200 as pkg
+    from paper_2510_00554_b200 import _native, device
+
+    assert torch.cuda.is_available(), "gpu tests need a CUDA device"
+    _native.load()          # the native library must be the thing that runs
+    return pkg
+
+
+def _alg(pkg, name):
+    return pkg.CompressionAlg.from_name(name)
+
+
+# ---- primitives ------------------------------------------------------------------
+
+def test_known_answers_through_hash_blocks(pkg, golden):
+    by_alg = {}
+    for rec in golden["kats"]:
+        data = rec["msg"].encode() if "msg" in rec else inputs.seeded_bytes(rec["seed"], rec["len"])
+        by_alg.setdefault(rec["alg"], []).append((data, rec["digest"]))
+    for alg, items in by_alg.items():
+        buf = pkg.hash_blocks(_alg(pkg, alg), [d for d, _ in items])
+        assert buf.count == len(items)
+        for i, (_, want) in enumerate(items):
+            assert buf.entry(i).hex() == want, (alg, i, len(items[i][0]))
+
+
+def test_compress_block_empty_and_abc(pkg):
+    assert pkg.compress_block(pkg.CompressionAlg.SHA256, b"").hex() == \
+        "e3b0c44298fc1c149afbf4c8996fb92427ae41e4649b934ca495991b7852b855"
+    assert pkg.compress_block(pkg.CompressionAlg.SHA3_256, b"abc").hex() == \
+        "3a985da74fe225b2045c172d6bd390bd855f086e3e9d525b46bfe24511431532"
+    assert len(pkg.compress_block(pkg.CompressionAlg.BLAKE2B, b"x").data) == 64
+
+
+def test_hash_blocks_unaligned_device_views(pkg, porc):
+    """Blocks addressed in place at every byte alignment and ragged length."""
+    from paper_2510_00554_b200 import device as dev
+
+    raw = inputs.seeded_bytes(77, 70_000)
+    base = dev.as_device_bytes(raw)
+    rng = np.random.default_rng(5)
+    offs = np.concatenate([np.arange(0, 40), rng.integers(0, 60_000, 200)]).astype(np.uint64)
+    lens = np.concatenate([np.arange(0, 40) * 7 % 300, rng.integers(0, 9000, 200)]).astype(np.uint64)
+    d_off = torch.from_numpy(offs.view(np.int64)).cuda()
+    d_len = torch.from_numpy(lens.view(np.int64)).cuda()
+    for alg in ALGS:
+        out = dev.hash_blocks_device(alg, base, d_off, d_len).cpu().numpy().tobytes()
+        dl = porc.DIGEST_LEN[alg]
+        for i, (o, l) in enumerate(zip(offs, lens)):
+            assert out[i * dl:(i + 1) * dl] == porc.h(alg, raw[int(o):int(o + l)]), (alg, i, int(o), int(l))
+
+
+def test_hash_blocks_zero_blocks_rejected(pkg):
+    with pytest.raises(pkg.errors.InvalidInput):
+        pkg.hash_blocks(pkg.CompressionAlg.SHA256, [])
+
+
+# ---- merkle ------------------------------------------------------------------------
+
+def test_merkle_roots_golden(pkg, golden):
+    for rec in golden["merkle"]:
+        alg = _alg(pkg, rec["alg"])
+        n = rec["n"]
+        leaves = inputs.seeded_bytes(rec["seed"], n * alg.digest_len)
+        buf = pkg.DigestBuffer(alg, bytearray(leaves), n)
+        assert pkg.merkle_root(alg, buf).hex() == rec["root"], (rec["alg"], n)
+
+
+def test_reduce_level_matches_oracle_and_state_machine(pkg, porc):
+    for name in ALGS:
+        alg = _alg(pkg, name)
+        for n in (2, 3, 8, 33):
+            leaves = inputs.seeded_bytes(600 + n, n * alg.digest_len)
+            state = pkg.ReductionState.from_leaves(pkg.DigestBuffer(alg, bytearray(leaves), n))
+            level, count = leaves, n
+            while count > 1:
+                got = pkg.reduce_level(state)
+                level = bytes(porc.reduce_level(name, level, count))
+                count = (count + 1) // 2
+                assert got == count
+                assert bytes(state.input_buffer.data[:count * alg.digest_len]) == level
+            with pytest.raises(pkg.errors.InvalidState):
+                pkg.reduce_level(state)
+
+
+def test_reduce_levels_forced_ranges(pkg, porc):
+    """The shard rule on the device: any aligned node range, any forced level count."""
+    from paper_2510_00554_b200 import device as dev
+
+    for name in ALGS:
+        dl = porc.DIGEST_LEN[name]
+        for n in (1, 5, 100, 1500, 5000):
+            leaves = inputs.seeded_bytes(900 + n, n * dl)
+            nodes = dev.as_device_bytes(leaves)
+            for levels in (1, 2, 3, 6, 10, 11, 13):
+                if levels > max(1, (n - 1).bit_length()) + 1:
+                    continue
+                width = 1 << levels
+                # whole range
+                got = dev.merkle_reduce_levels_device(name, nodes, 0, n, n, levels).cpu().numpy().tobytes()
+                want = porc.reduce_levels_forced(name, leaves, 0, n, n, levels)
+                assert got == want, (name, n, levels)
+                # a sub-range starting on a shard boundary
+                if n > 2 * width:
+                    first = width
+                    n_in = min(n - first, 2 * width) if (n - first) >= 2 * width else n - first
+                    sub = dev.as_device_bytes(leaves[first * dl:(first + n_in) * dl])
+                    got = dev.merkle_reduce_levels_device(name, sub, first, n_in, n, levels).cpu().numpy().tobytes()
+                    want = porc.reduce_levels_forced(name, leaves[first * dl:(first + n_in) * dl], first, n_in, n, levels)
+                    assert got == want, (name, n, levels, "sub")
+
+
+# ---- models --------------------------------------------------------------------------
+
+def test_reference_suite_golden_inplace_digest(pkg):
+    import random
+
+    rng = random.Random(2024)
+    model = pkg.TensorMap([(f"t{i}", rng.randbytes(s)) for i, s in enumerate([100, 8192, 5000, 0, 20000])])
+    res = pkg.hash_model(pkg.HashConfig(pkg.Construction.MERKLE, pkg.Strategy.IN_PLACE), model)
+    assert res.digest_hex() == "5d70823521307e19d8a9451a8c264c8cd156ee99a9d7f46e9406867d712c9a7e"
+    assert res.block_count == 6
+    assert res.layer_digests is None and res.aux_data_bytes == 0
+
+
+def test_seeded_models_root_and_every_leaf(pkg, golden):
+    from paper_2510_00554_b200 import device as dev
+
+    for rec in golden["models"]:
+        if rec["kind"] != "seeded":
+            continue
+        tensors = inputs.model_tensors(rec["seed"], rec["sizes"])
+        model = pkg.TensorMap([(f"t{i}", t) for i, t in enumerate(tensors)])
+        bs = rec["block_size"]
+        for name in ALGS:
+            cfg = pkg.HashConfig(pkg.Construction.MERKLE, pkg.Strategy.IN_PLACE, _alg(pkg, name), bs)
+            res = pkg.hash_model(cfg, model)
+            assert res.digest_hex() == rec[f"merkle_inplace_{name}"], (rec["case"], bs, name)
+            assert res.block_count == rec["n_blocks"]
+            plan = dev.ModelPlan([dev.as_device_bytes(t) for t in tensors], bs)
+            hasher = dev.MerkleModelHasher(plan, name)
+            hasher.run()
+            assert hashlib.sha256(hasher.leaf_bytes()).hexdigest() == rec[f"leaves_sha256_{name}"]
+            assert hasher.out_bytes().hex() == rec[f"merkle_inplace_{name}"]
+            cfg_c = pkg.HashConfig(pkg.Construction.MERKLE, pkg.Strategy.COALESCED, _alg(pkg, name), bs)
+            assert pkg.hash_model(cfg_c, model).digest_hex() == rec[f"merkle_coalesced_{name}"]
+        lat = pkg.HashConfig(pkg.Construction.LATTICE, pkg.Strategy.IN_PLACE, pkg.CompressionAlg.BLAKE2B, bs)
+        assert pkg.hash_model(lat, model).digest_hex() == rec["lattice_inplace"], (rec["case"], bs)
+        lat_c = pkg.HashConfig(pkg.Construction.LATTICE, pkg.Strategy.COALESCED, pkg.CompressionAlg.BLAKE2B, bs)
+        assert pkg.hash_model(lat_c, model).digest_hex() == rec["lattice_coalesced"]
+
+
+def test_unaligned_device_tensors_hashed_in_place(pkg, porc):
+    """Views at 1-, 2-, 4-, 8-byte offsets into one allocation (storage offsets of real checkpoints)."""
+    raw = inputs.seeded_bytes(31, 200_000)
+    base = torch.frombuffer(bytearray(raw), dtype=torch.uint8).cuda()
+    cuts = [(1, 9000), (9003, 8192), (17200, 33000), (50204, 1), (50208, 70000), (120216, 16384)]
+    entries = [(f"v{i}", base[o:o + l]) for i, (o, l) in enumerate(cuts)]
+    host = [raw[o:o + l] for o, l in cuts]
+    for name in ALGS:
+        for bs in (64, 8192):
+            cfg = pkg.HashConfig(pkg.Construction.MERKLE, pkg.Strategy.IN_PLACE, _alg(pkg, name), bs)
+            assert pkg.hash_model(cfg, pkg.TensorMap(entries)).model_digest.data == porc.inplace_merkle(name, host, bs)
+    cfg = pkg.HashConfig(pkg.Construction.LATTICE, pkg.Strategy.IN_PLACE, pkg.CompressionAlg.BLAKE2B, 1024)
+    assert pkg.hash_model(cfg, pkg.TensorMap(entries)).model_digest.data == porc.inplace_lattice(host, 1024)
+
+
+def test_empty_model_and_bad_config(pkg):
+    cfg = pkg.HashConfig(pkg.Construction.MERKLE, pkg.Strategy.IN_PLACE)
+    with pytest.raises(pkg.errors.InvalidInput):
+        pkg.hash_model(cfg, pkg.TensorMap([("a", b"")]))
+    with pytest.raises(pkg.errors.InvalidInput):
+        pkg.hash_model(cfg, pkg.TensorMap([]))
+    with pytest.raises(pkg.errors.ConfigError):
+        pkg.hash_model(pkg.HashConfig(pkg.Construction.LATTICE, pkg.Strategy.IN_PLACE, pkg.CompressionAlg.SHA256),
+                       pkg.TensorMap([("a", b"x")]))
+    single = pkg.hash_model(cfg, pkg.TensorMap([("t", b"z" * 100)]))
+    assert single.model_digest.data == hashlib.sha256(b"z" * 100).digest() and single.block_count == 1
+
+
+def _synthetic(arch, scale=1.0):
+    from paper_2510_00554_b200 import shapes
+
+    return shapes.synthetic_state_dict(arch, torch.device("cuda"), seed=0, scale=scale)
+
+
+@pytest.mark.parametrize("arch,alg", [("gpt2", "sha256"), ("vgg19", "blake2b"), ("vgg19", "sha3-256")])
+def test_full_size_models_against_c_oracle(pkg, corc, arch, alg):
+    """BASELINE configs 1 and 4 at full size: root AND every leaf digest, bit-exact."""
+    from paper_2510_00554_b200 import device as dev
+
+    sd = _synthetic(arch)
+    flat = [dev.as_device_bytes(t) for _, t in sd]
+    plan = dev.ModelPlan(flat, 8192)
+    hasher = dev.MerkleModelHasher(plan, alg)
+    hasher.run()
+    host = [t.cpu().numpy() for t in flat]
+    tl = corc.TensorList(host)
+    threads = corc.threads_default()
+    want_leaves = corc.inplace_leaves(alg, tl, 8192, threads)
+    assert plan.leaf_count * corc.DLEN[alg] == len(want_leaves)
+    got_leaves = hasher.leaf_bytes()
+    assert got_leaves == want_leaves
+    assert hasher.out_bytes() == corc.merkle_root(alg, want_leaves, plan.leaf_count, threads)
+    # the reference-shaped API gives the same root
+    cfg = pkg.HashConfig(pkg.Construction.MERKLE, pkg.Strategy.IN_PLACE, _alg(pkg, alg), 8192)
+    res = pkg.hash_model(cfg, pkg.TensorMap(list(sd)))
+    assert res.model_digest.data == hasher.out_bytes()
+
+
+def test_shard_roots_recombine_to_whole_root(pkg):
+    """Size-independent property of the multi-GPU rule, on one GPU at GPT-2-small size."""
+    from paper_2510_00554_b200 import device as dev
+    from paper_2510_00554_b200 import distributed as dd
+
+    sd = _synthetic("gpt2")
+    plan = dev.ModelPlan([dev.as_device_bytes(t) for _, t in sd], 8192)
+    for alg in ("sha256", "blake2b"):
+        whole = dev.MerkleModelHasher(plan, alg)
+        whole.run()
+        root = whole.out_bytes()
+        for world in (2, 3, 8):
+            sp = dd.plan_shards(plan.leaf_count, world)
+            parts = []
+            for rank in range(world):
+                a, b = sp.leaf_range(rank)
+                if b > a:
+                    h = dev.MerkleModelHasher(plan, alg, a, b, sp.levels)
+                    h.run()
+                    parts.append(h.out)
+            nodes = torch.cat(parts)
+            assert nodes.numel() == sp.n_shards * dev.DIGEST_LEN[alg]
+            assert dev.merkle_root_device(alg, nodes, sp.n_shards).cpu().numpy().tobytes() == root, (alg, world)
+
+
+# ---- lattice / dataset -------------------------------------------------------------------
+
+def test_lattice_vectors(pkg, golden):
+    lat = golden["lattice"]
+    for rec in lat["hash_block"]:
+        data = inputs.seeded_bytes(rec["seed"], rec["len"])
+        assert pkg.lt_hash_block(rec["index"], data).hex() == rec["digest"], rec
+    for rec in lat["tagged"]:
+        tag = inputs.seeded_bytes(rec["tag_seed"], rec["tag_len"])
+        data = inputs.seeded_bytes(rec["seed"], rec["len"])
+        assert pkg.lattice.lt_hash_tagged(tag, data).hex() == rec["digest"]
+    for rec in lat["reduce"]:
+        ds = [pkg.LatticeDigest(inputs.seeded_bytes(rec["seed_base"] + i, 64)) for i in range(rec["n"])]
+        assert pkg.lt_reduce(ds).hex() == rec["sum"]
+        assert pkg.lattice.lt_reduce_pairwise(ds).hex() == rec["sum"]
+    assert pkg.lt_reduce([]).data == bytes(64)
+    assert pkg.lt_hash_block(0, b"").data == hashlib.blake2b(bytes(8)).digest()
+
+
+def test_dataset_golden_process_batch_and_device_path(pkg, golden, tmp_path):
+    for rec in golden["datasets"]:
+        spec = inputs.DATASET_CASES[rec["case"]]
+        samples = inputs.dataset_samples(**spec)
+        want = {int(k): (v[0], v[1]) for k, v in rec["digests"].items()}
+        # (a) the reference's host-object protocol, batch by batch
+        acc = pkg.SourceAccumulator(cover_labels=rec["cover_labels"])
+        acc.declare(spec["declared"])
+        recs = [pkg.SampleRecord(*s) for s in samples]
+        for start in range(0, len(recs), 50):
+            pkg.process_batch(pkg.Batch(recs[start:start + 50]), acc)
+        got = {sid: (d.hex(), c) for sid, (d, c) in pkg.finalize(acc).items()}
+        assert got == want
+        # (b) manifest -> digest_dataset (whole shard resident, one launch)
+        shard, off, ln, ids, src = inputs.pack_samples(samples)
+        rows = [(int(ids[i]), int(src[i]), samples[i][2], int(off[i]), int(ln[i])) for i in range(len(samples))]
+        man = pkg.DatasetManifest(rows, tmp_path / "shard.bin")
+        man.save(tmp_path / "m.json", shard)
+        loaded = pkg.DatasetManifest.load(tmp_path / "m.json")
+        got = {sid: (d.hex(), c) for sid, (d, c) in
+               pkg.digest_dataset(loaded, batch_size=13, shuffle_seed=4, cover_labels=rec["cover_labels"]).items()}
+        assert got == {sid: v for sid, v in want.items() if sid in loaded.source_ids}
+
+
+def test_undeclared_source_rejected(pkg):
+    acc = pkg.SourceAccumulator()
+    acc.declare([1, 2])
+    with pytest.raises(pkg.errors.ValidationError):
+        pkg.process_batch(pkg.Batch([pkg.SampleRecord(5, 3, b"", b"abc")]), acc)
+
+
+def test_cifar_shaped_dataset_against_c_oracle(pkg, corc):
+    """BASELINE config 3 at full size: 50,000 x 3,072-byte samples, 16 sources, every sample digest."""
+    from paper_2510_00554_b200 import dataset as ds
+    from paper_2510_00554_b200 import device as dev
+
+    n, ln, n_src = 50_000, 3072, 16
+    rng = np.random.default_rng(0)
+    shard = rng.integers(0, 256, size=n * ln, dtype=np.uint8)
+    ids = np.arange(n, dtype=np.uint64)
+    probs = np.random.default_rng(1).dirichlet(np.ones(n_src))
+    src = np.random.default_rng(1).choice(n_src, size=n, p=probs)
+    offs = (np.arange(n, dtype=np.uint64) * ln)
+    lens = np.full(n, ln, dtype=np.uint64)
+    dset = ds.DeviceDataset.from_host(shard, offs, lens, ids, src, list(range(n_src)))
+    acc = dev.LatticeAccumulator(n_src)
+    per_sample = torch.empty(n * 64, dtype=torch.uint8, device="cuda")
+    dset.accumulate(acc, digests=per_sample)
+    out, counts, status = acc.digests()
+    want_sums, want_counts, want_digests = corc.lthash_samples(shard, offs, lens, ids, src.astype(np.uint32), n_src,
+                                                               corc.threads_default(), want_digests=True)
+    assert status == 0
+    assert per_sample.cpu().numpy().tobytes() == want_digests
+    assert out == want_sums and counts == want_counts
+    # split into ranges (the multi-GPU partition) and accumulate: same sums
+    acc2 = dev.LatticeAccumulator(n_src)
+    for a, b in [(0, 7), (7, 20_001), (20_001, n)]:
+        dset.accumulate(acc2, a, b)
+    assert acc2.digests()[:2] == (want_sums, want_counts)
+
+
+def test_hellaswag_shaped_variable_length_samples(pkg, corc):
+    """BASELINE config 5 shape: 4*len-byte int32 token arrays, ragged, hashed at true length."""
+    from paper_2510_00554_b200 import dataset as ds
+    from paper_2510_00554_b200 import device as dev
+
+    n, n_src = 4000, 16
+    rng = np.random.default_rng(2)
+    toks = np.clip(np.round(rng.lognormal(np.log(90), 0.4, size=n)), 16, 256).astype(np.int64)
+    lens = (toks * 4).astype(np.uint64)
+    offs = np.zeros(n, dtype=np.uint64)
+    np.cumsum(lens[:-1], out=offs[1:])
+    shard = rng.integers(0, 50257, size=int(toks.sum()), dtype=np.int32).view(np.uint8)
+    src = np.random.default_rng(3).integers(0, n_src, size=n)
+    ids = np.arange(n, dtype=np.uint64) * 7 + 3
+    dset = ds.DeviceDataset.from_host(shard, offs, lens, ids, src, list(range(n_src)))
+    acc = dev.LatticeAccumulator(n_src)
+    dset.accumulate(acc)
+    out, counts, _ = acc.digests()
+    want_sums, want_counts = corc.lthash_samples(shard, offs, lens, ids, src.astype(np.uint32), n_src, 4)
+    assert out == want_sums and counts == want_counts
+
+
+def test_many_sources_take_the_global_accumulator_path(pkg, corc):
+    from paper_2510_00554_b200 import dataset as ds
+    from paper_2510_00554_b200 import device as dev
+
+    n, n_src = 3000, 300           # > LT_SMEM_SOURCES
+    rng = np.random.default_rng(9)
+    lens = rng.integers(0, 400, size=n).astype(np.uint64)
+    offs = np.zeros(n, dtype=np.uint64)
+    np.cumsum(lens[:-1], out=offs[1:])
+    shard = rng.integers(0, 256, size=int(lens.sum()) + 16, dtype=np.uint8)
+    src = rng.integers(0, n_src, size=n)
+    ids = rng.integers(0, 2**63, size=n).astype(np.uint64)
+    dset = ds.DeviceDataset.from_host(shard, offs, lens, ids, src, list(range(n_src)))
+    acc = dev.LatticeAccumulator(n_src)
+    dset.accumulate(acc)
+    out, counts, _ = acc.digests()
+    want_sums, want_counts = corc.lthash_samples(shard, offs, lens, ids, src.astype(np.uint32), n_src, 2)
+    assert out == want_sums and counts == want_counts
+
+
+def test_sign_and_verify_gpu_digests_end_to_end(pkg):
+    """Config 5's last step: digest on the GPU, sign and verify on the host."""
+    import random
+
+    rng = random.Random(3)
+    model = pkg.TensorMap([(f"l{i}", rng.randbytes(rng.randint(1, 30000))) for i in range(5)])
+    cfg = pkg.HashConfig(pkg.Construction.MERKLE, pkg.Strategy.IN_PLACE)
+    res = pkg.hash_model(cfg, model)
+    key = pkg.keygen()
+    stmt = pkg.Statement([pkg.Subject("m", {cfg.alg.value: res.digest_hex()})],
+                         pkg.attestation.MODEL_PREDICATE_TYPE, cfg.predicate())
+    bundle = pkg.sign_bundle(stmt, key)
+    replay = pkg.HashConfig.from_predicate(bundle.statement().predicate)
+    again = pkg.hash_model(replay, model)
+    assert pkg.verify_bundle(bundle, {"m": {cfg.alg.value: again.digest_hex()}}) is pkg.Verdict.OK
+    tampered = pkg.TensorMap([(n, (b[:-1] + bytes([b[-1] ^ 1])) if n == "l2" else b) for n, b in model.entries])
+    bad = pkg.hash_model(replay, tampered)
+    assert pkg.verify_bundle(bundle, {"m": {cfg.alg.value: bad.digest_hex()}}) is pkg.Verdict.DIGEST_MISMATCH
