@@ -50,6 +50,7 @@ def parse_args():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-dataset", action="store_true")
+    ap.add_argument("--no-intpeak", action="store_true")
     ap.add_argument("--cpu-sample-mb", type=int, default=1024)
     return ap.parse_args()
 
@@ -284,7 +285,7 @@ def run_ours(args):
     # ---- integer-pipe roofline: measured on this box by tools/intpeak
     int_pipe = None
     intpeak_bin = ROOT / "tools" / "_build" / "intpeak"
-    if rank == 0 and intpeak_bin.exists() and args.alg == "sha256":
+    if rank == 0 and intpeak_bin.exists() and args.alg == "sha256" and not args.no_intpeak:
         try:
             out = subprocess.run([str(intpeak_bin)], capture_output=True, text=True, timeout=120).stdout
             peaks = json.loads(out.strip().splitlines()[-1])
