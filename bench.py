@@ -416,7 +416,9 @@ def run_ours(args):
 
     if rank == 0:
         line = {
-            "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "metric": METRIC if (args.arch, args.alg) == ("gpt2-xl", "sha256")
+            else f"{args.arch}_{args.alg}_merkle_inplace_hash_throughput".replace("-", ""),
+            "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
             "config": {"workload": WORKLOAD if args.arch == "gpt2-xl" and args.alg == "sha256"

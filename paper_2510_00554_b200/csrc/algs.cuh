@@ -16,6 +16,7 @@ namespace snt {
 struct MerkleConsts {
     uint32_t sha256_pad_leaf[64];   // K+W of the padding block after a full leaf
     uint32_t sha256_pad_node[64];   // K+W of the padding block after a 64-byte node message
+    uint32_t one;                   // 1, opaque to the compiler (Sha256::add_fma)
 };
 
 template <int ALG> struct AlgTraits;
@@ -26,11 +27,11 @@ template <> struct AlgTraits<ALG_SHA256> {
     // carrier words -> little-endian memory words and back
     SNT_HD static uint32_t to_mem(uint32_t w) { return bswap32(w); }
     SNT_HD static uint32_t from_mem(uint32_t w) { return bswap32(w); }
-    SNT_HD static void leaf(const uint8_t* p, uint64_t len, uint32_t d[DW]) {
-        Sha256::hash_message(p, len, d);
+    SNT_HD static void leaf(const uint8_t* p, uint64_t len, const MerkleConsts& c, uint32_t d[DW]) {
+        Sha256::hash_message(p, len, d, c.one);
     }
     SNT_HD static void pair(const uint32_t* l, const uint32_t* r, const MerkleConsts& c, uint32_t* out) {
-        Sha256::hash_pair(l, r, c.sha256_pad_node, out);
+        Sha256::hash_pair(l, r, c.sha256_pad_node, out, c.one);
     }
 };
 
@@ -39,7 +40,7 @@ template <> struct AlgTraits<ALG_BLAKE2B> {
     static constexpr int DW = 16;
     SNT_HD static uint32_t to_mem(uint32_t w) { return w; }
     SNT_HD static uint32_t from_mem(uint32_t w) { return w; }
-    SNT_HD static void leaf(const uint8_t* p, uint64_t len, uint32_t d[DW]) {
+    SNT_HD static void leaf(const uint8_t* p, uint64_t len, const MerkleConsts&, uint32_t d[DW]) {
         uint64_t h[8];
         Blake2b::hash_message<0>(0, 0, p, len, h);
 #pragma unroll
@@ -63,7 +64,7 @@ template <> struct AlgTraits<ALG_SHA3_256> {
     static constexpr int DW = 8;
     SNT_HD static uint32_t to_mem(uint32_t w) { return w; }
     SNT_HD static uint32_t from_mem(uint32_t w) { return w; }
-    SNT_HD static void leaf(const uint8_t* p, uint64_t len, uint32_t d[DW]) {
+    SNT_HD static void leaf(const uint8_t* p, uint64_t len, const MerkleConsts&, uint32_t d[DW]) {
         uint64_t h[4];
         Sha3_256::hash_message(p, len, h);
 #pragma unroll

@@ -43,11 +43,16 @@ uint64_t cdiv_shift(uint64_t n, uint32_t s) { return ceil_shift(n, s); }
 
 bool valid_alg(int alg) { return alg == SNT_SHA256 || alg == SNT_BLAKE2B || alg == SNT_SHA3_256; }
 
+uint32_t max_levels(int alg) {
+    return alg == SNT_BLAKE2B ? ReduceShape<ALG_BLAKE2B>::MAX_LEVELS : ReduceShape<ALG_SHA256>::MAX_LEVELS;
+}
+
 const MerkleConsts& node_consts() {
     static const MerkleConsts c = [] {
         MerkleConsts k;
         memset(&k, 0, sizeof(k));
         Sha256::pad_schedule(64, k.sha256_pad_node);
+        k.one = 1;
         return k;
     }();
     return c;
@@ -154,9 +159,9 @@ uint64_t snt_model_plan_total_bytes(const snt_model_plan* plan) { return plan ? 
 
 size_t snt_merkle_work_bytes(int alg, uint64_t count) {
     // two ping-pong buffers, each able to hold the widest intermediate level:
-    // every launch but the last folds REDUCE_MAX_LEVELS levels, so the widest
-    // intermediate has ceil(count / 2^REDUCE_MAX_LEVELS) nodes
-    return 2 * static_cast<size_t>(cdiv_shift(count, REDUCE_MAX_LEVELS) + 1) * snt_digest_len(alg);
+    // every launch but the last folds max_levels(alg) levels, so the widest
+    // intermediate has ceil(count / 2^max_levels) nodes
+    return 2 * static_cast<size_t>(cdiv_shift(count, max_levels(alg)) + 1) * snt_digest_len(alg);
 }
 
 }  // extern "C"
@@ -184,7 +189,7 @@ int launch_reduce_alg(int alg, const uint8_t* in, uint64_t first, uint64_t n_in,
     }
 }
 
-// Apply `levels` levels to the node range, REDUCE_MAX_LEVELS at a time,
+// Apply `levels` levels to the node range, max_levels(alg) at a time,
 // ping-ponging intermediates through `work`; the last launch writes `out`.
 int reduce_chain(int alg, const uint8_t* in, uint64_t first, uint64_t n_in, uint64_t level_count,
                  uint32_t levels, uint8_t* work, size_t work_bytes, uint8_t* out,
@@ -194,7 +199,8 @@ int reduce_chain(int alg, const uint8_t* in, uint64_t first, uint64_t n_in, uint
     int flip = 0;
     const uint8_t* src = in;
     while (levels > 0) {
-        const uint32_t m = levels < static_cast<uint32_t>(REDUCE_MAX_LEVELS) ? levels : REDUCE_MAX_LEVELS;
+        const uint32_t cap = max_levels(alg);
+        const uint32_t m = levels < cap ? levels : cap;
         const uint64_t n_out = cdiv_shift(n_in, m);
         uint8_t* dst = out;
         if (levels > m) {
@@ -231,7 +237,7 @@ int launch_blocks(const uint8_t* base, const uint64_t* off, const uint64_t* len,
                   uint8_t* out, cudaStream_t s) {
     const uint64_t grid = (n + LEAF_THREADS - 1) / LEAF_THREADS;
     if (grid > 0x7fffffffull) return SNT_ERR_INVALID_INPUT;
-    hash_blocks_kernel<ALG><<<static_cast<unsigned>(grid), LEAF_THREADS, 0, s>>>(base, off, len, n, out);
+    hash_blocks_kernel<ALG><<<static_cast<unsigned>(grid), LEAF_THREADS, 0, s>>>(base, off, len, n, node_consts(), out);
     SNT_CUDA(cudaGetLastError());
     ++g_launches;
     return SNT_OK;

@@ -14,8 +14,6 @@ namespace snt {
 
 constexpr int LEAF_THREADS = 128;
 constexpr int REDUCE_THREADS = 256;
-constexpr int REDUCE_LOCAL_LEVELS = 2;                       // 4 digests per thread
-constexpr int REDUCE_MAX_LEVELS = REDUCE_LOCAL_LEVELS + 8;   // 1024 digests per CTA
 
 // ---- leaf hashing -----------------------------------------------------------
 
@@ -23,7 +21,7 @@ constexpr int REDUCE_MAX_LEVELS = REDUCE_LOCAL_LEVELS + 8;   // 1024 digests per
 // 16-byte aligned: 4 x LDG.128 per compression with the next block's loads
 // issued before the current block's rounds, then the constant padding block.
 SNT_HD void sha256_leaf_aligned(const uint8_t* __restrict__ p, uint32_t nblk,
-                               const uint32_t* __restrict__ pad_kw, uint32_t s[8]) {
+                               const uint32_t* __restrict__ pad_kw, uint32_t s[8], uint32_t one = 1u) {
     Sha256::init(s);
     U4 q0 = ld128(p), q1 = ld128(p + 16), q2 = ld128(p + 32), q3 = ld128(p + 48);
 #pragma unroll 1
@@ -37,7 +35,7 @@ SNT_HD void sha256_leaf_aligned(const uint8_t* __restrict__ p, uint32_t nblk,
             const uint8_t* n = p + (static_cast<size_t>(b + 1) << 6);
             q0 = ld128(n); q1 = ld128(n + 16); q2 = ld128(n + 32); q3 = ld128(n + 48);
         }
-        Sha256::compress(s, w);
+        Sha256::compress(s, w, one);
     }
     Sha256::compress_const(s, pad_kw);
 }
@@ -81,12 +79,12 @@ merkle_leaf_kernel(const TensorTable tab, const __grid_constant__ MerkleConsts c
         const bool fast = exists && leaf.len == (1ull << tab.block_shift) &&
                           (reinterpret_cast<uintptr_t>(leaf.ptr) & 15) == 0;
         if (__all_sync(0xffffffffu, fast)) {
-            sha256_leaf_aligned(leaf.ptr, 1u << (tab.block_shift - 6), c.sha256_pad_leaf, d);
+            sha256_leaf_aligned(leaf.ptr, 1u << (tab.block_shift - 6), c.sha256_pad_leaf, d, c.one);
         } else if (exists) {
-            A::leaf(leaf.ptr, leaf.len, d);
+            A::leaf(leaf.ptr, leaf.len, c, d);
         }
     } else {
-        if (exists) A::leaf(leaf.ptr, leaf.len, d);
+        if (exists) A::leaf(leaf.ptr, leaf.len, c, d);
     }
     if (exists) store_digest<ALG>(d_leaves + (k - leaf_begin) * A::DIGEST_BYTES, d);
 }
@@ -96,12 +94,13 @@ merkle_leaf_kernel(const TensorTable tab, const __grid_constant__ MerkleConsts c
 template <int ALG>
 __global__ void __launch_bounds__(LEAF_THREADS)
 hash_blocks_kernel(const uint8_t* __restrict__ base, const uint64_t* __restrict__ off,
-                   const uint64_t* __restrict__ len, uint64_t n, uint8_t* __restrict__ out) {
+                   const uint64_t* __restrict__ len, uint64_t n, const __grid_constant__ MerkleConsts c,
+                   uint8_t* __restrict__ out) {
     using A = AlgTraits<ALG>;
     const uint64_t i = static_cast<uint64_t>(blockIdx.x) * LEAF_THREADS + threadIdx.x;
     if (i >= n) return;
     uint32_t d[A::DW];
-    A::leaf(base + off[i], len[i], d);
+    A::leaf(base + off[i], len[i], c, d);
     store_digest<ALG>(out + i * A::DIGEST_BYTES, d);
 }
 
@@ -110,11 +109,25 @@ hash_blocks_kernel(const uint8_t* __restrict__ base, const uint64_t* __restrict_
 // Input: nodes of one tree level with global indices [first, first + n_in);
 // `level_count` is the number of nodes the whole tree has at that level (a
 // node index >= level_count does not exist and pairs as zeros). Each CTA
-// applies `levels` (1..REDUCE_MAX_LEVELS) levels to its aligned group of
+// applies `levels` (1..reduce_max_levels) levels to its aligned group of
 // 2^levels inputs and writes one node. Levels are never skipped: a group that
 // is down to one node keeps pairing it with zeros, which is exactly what the
 // reference tree does to the last node of every odd level and what makes
 // per-shard roots combine into the reference root.
+//
+// Work layout: level by level through shared memory with the active threads
+// compacted -- at every level thread p hashes pair p, so the wide bottom
+// levels (where almost all the node hashes are) run with full warps: a
+// 1024-node group costs 36 warp-hash-times against the ideal 32, and the
+// critical path is one node hash per level. Digests sit in shared memory word
+// by word ([word][node]) so that the pair loads are conflict-free 64-bit reads.
+
+template <int ALG>
+struct ReduceShape {
+    static constexpr int DW = AlgTraits<ALG>::DW;
+    static constexpr int CAP = (DW == 8) ? 512 : 256;     // level-1 outputs held per CTA
+    static constexpr int MAX_LEVELS = (DW == 8) ? 10 : 9; // 2 * CAP inputs per CTA
+};
 
 template <int ALG>
 SNT_D void pair_or_pad(uint32_t* left, const uint32_t* right, bool right_exists,
@@ -129,26 +142,6 @@ SNT_D void pair_or_pad(uint32_t* left, const uint32_t* right, bool right_exists,
     for (int i = 0; i < A::DW; ++i) left[i] = out[i];
 }
 
-// `nlev` shuffle levels inside a warp. Lane l holds node index g (at relative
-// level t) when l is a multiple of `stride`; holders that are multiples of
-// 2*stride become the parents.
-template <int ALG>
-SNT_D void warp_levels(uint32_t* d, uint64_t& g, uint32_t& t, uint32_t nlev, uint32_t stride0,
-                       uint64_t level_count, const MerkleConsts& c) {
-    using A = AlgTraits<ALG>;
-    uint32_t stride = stride0;
-    for (uint32_t s = 0; s < nlev; ++s) {
-        uint32_t r[A::DW];
-#pragma unroll
-        for (int i = 0; i < A::DW; ++i) r[i] = __shfl_down_sync(0xffffffffu, d[i], stride);
-        const bool right_exists = (g + 1) < ceil_shift(level_count, t);
-        pair_or_pad<ALG>(d, r, right_exists, c);
-        g >>= 1;
-        t += 1;
-        stride <<= 1;
-    }
-}
-
 template <int ALG>
 __global__ void __launch_bounds__(REDUCE_THREADS)
 merkle_reduce_kernel(const uint8_t* __restrict__ in, uint64_t first, uint64_t n_in,
@@ -156,69 +149,62 @@ merkle_reduce_kernel(const uint8_t* __restrict__ in, uint64_t first, uint64_t n_
                      uint8_t* __restrict__ out) {
     using A = AlgTraits<ALG>;
     constexpr int DW = A::DW;
-    __shared__ uint32_t xwarp[REDUCE_THREADS / 32][DW];
+    constexpr int CAP = ReduceShape<ALG>::CAP;
+    __shared__ uint32_t buf_a[DW * CAP];
+    __shared__ uint32_t buf_b[DW * CAP / 2];
 
-    const uint32_t a = levels < REDUCE_LOCAL_LEVELS ? levels : REDUCE_LOCAL_LEVELS;  // thread-local levels
-    const uint32_t r = levels - a;                                                    // cooperative levels
-    const uint32_t nthreads = 1u << r;                                                // threads holding data
     const uint32_t tid = threadIdx.x;
-    const uint32_t lane = tid & 31;
-
-    // node index (at the input level) of this thread's first input
-    const uint64_t gi = first + (static_cast<uint64_t>(blockIdx.x) << levels) +
-                        (static_cast<uint64_t>(tid) << a);
+    const uint64_t base = first + (static_cast<uint64_t>(blockIdx.x) << levels);   // first input of this CTA
     const uint64_t in_end = first + n_in;
+    const uint32_t width = 1u << levels;
 
-    uint32_t d[DW];
+    // level 0 -> 1 straight from global memory: pair p = inputs base + 2p, base + 2p + 1
+    for (uint32_t p = tid; p < (width >> 1); p += REDUCE_THREADS) {
+        const uint64_t g = base + 2ull * p;
+        if (g < in_end) {
+            uint32_t l[DW], r[DW];
+            load_digest<ALG>(in + (g - first) * A::DIGEST_BYTES, l);
+            const bool r_exists = g + 1 < in_end;
+            if (r_exists) load_digest<ALG>(in + (g + 1 - first) * A::DIGEST_BYTES, r);
+            pair_or_pad<ALG>(l, r, r_exists, c);
 #pragma unroll
-    for (int i = 0; i < DW; ++i) d[i] = 0;
-    uint64_t g = gi;      // index of the node this thread holds, at relative level t
-    uint32_t t = 0;
-
-    if (tid < nthreads) {
-        // thread-local subtree over 2^a consecutive inputs
-        uint32_t n1[DW], n2[DW], n3[DW];
-        const bool e0 = gi < in_end;
-        if (e0) load_digest<ALG>(in + (gi - first) * A::DIGEST_BYTES, d);
-        if (a >= 1) {
-            const bool e1 = gi + 1 < in_end;
-            if (e1) load_digest<ALG>(in + (gi + 1 - first) * A::DIGEST_BYTES, n1);
-            if (a >= 2) {
-                const bool e2 = gi + 2 < in_end, e3 = gi + 3 < in_end;
-                if (e2) load_digest<ALG>(in + (gi + 2 - first) * A::DIGEST_BYTES, n2);
-                if (e3) load_digest<ALG>(in + (gi + 3 - first) * A::DIGEST_BYTES, n3);
-                if (e2) pair_or_pad<ALG>(n2, n3, e3, c);
-            }
-            if (e0) pair_or_pad<ALG>(d, n1, e1, c);
-            if (a >= 2) {
-                // level 1 -> 2: right child (gi>>1)+1 exists iff it is inside the tree
-                const bool r_exists = ((gi >> 1) + 1) < ceil_shift(level_count, 1);
-                if (e0) pair_or_pad<ALG>(d, n2, r_exists, c);
-            }
+            for (int i = 0; i < DW; ++i) buf_a[i * CAP + p] = l[i];
         }
     }
-    g = gi >> a;
-    t = a;
+    __syncthreads();
 
-    if (r > 0) {
-        const uint32_t wl = r < 5 ? r : 5;
-        warp_levels<ALG>(d, g, t, wl, 1, level_count, c);
-        if (r > 5) {
-            if (lane == 0) {
+    uint32_t* src = buf_a;
+    uint32_t* dst = buf_b;
+    uint32_t src_stride = CAP, dst_stride = CAP / 2;
+    for (uint32_t t = 1; t < levels; ++t) {
+        const uint32_t n_out = width >> (t + 1);
+        const uint64_t cnt = ceil_shift(level_count, t);          // nodes the tree has at this level
+        const uint64_t gbase = base >> t;
+        for (uint32_t p = tid; p < n_out; p += REDUCE_THREADS) {
+            const uint64_t g = gbase + 2ull * p;
+            if (g < cnt) {
+                uint32_t l[DW], r[DW];
 #pragma unroll
-                for (int i = 0; i < DW; ++i) xwarp[tid >> 5][i] = d[i];
-            }
-            __syncthreads();
-            if (tid < 32) {
-                const uint32_t nw = nthreads >> 5;    // warps that held data (2, 4 or 8)
+                for (int i = 0; i < DW; ++i) {
+                    const uint2 v = *reinterpret_cast<const uint2*>(src + i * src_stride + 2 * p);
+                    l[i] = v.x;
+                    r[i] = v.y;
+                }
+                pair_or_pad<ALG>(l, r, g + 1 < cnt, c);
 #pragma unroll
-                for (int i = 0; i < DW; ++i) d[i] = lane < nw ? xwarp[lane][i] : 0u;
-                g = ((first + (static_cast<uint64_t>(blockIdx.x) << levels)) >> t) + lane;
-                warp_levels<ALG>(d, g, t, r - 5, 1, level_count, c);
+                for (int i = 0; i < DW; ++i) dst[i * dst_stride + p] = l[i];
             }
         }
+        __syncthreads();
+        uint32_t* tp = src; src = dst; dst = tp;
+        const uint32_t ts = src_stride; src_stride = dst_stride; dst_stride = ts;
     }
-    if (tid == 0) store_digest<ALG>(out + static_cast<uint64_t>(blockIdx.x) * A::DIGEST_BYTES, d);
+    if (tid == 0) {
+        uint32_t d[DW];
+#pragma unroll
+        for (int i = 0; i < DW; ++i) d[i] = src[i * src_stride];
+        store_digest<ALG>(out + static_cast<uint64_t>(blockIdx.x) * A::DIGEST_BYTES, d);
+    }
 }
 
 }  // namespace snt

@@ -21,6 +21,21 @@ struct Sha256 {
     SNT_HD static uint32_t ch(uint32_t e, uint32_t f, uint32_t g) { return (e & f) ^ (~e & g); }
     SNT_HD static uint32_t maj(uint32_t a, uint32_t b, uint32_t c) { return (a & b) ^ (a & c) ^ (b & c); }
 
+    // a + b on the FMA pipe (IMAD): `one` is a runtime 1 the compiler cannot fold,
+    // so the add stays an integer multiply-add instead of an ALU-pipe IADD3. The
+    // leaf kernel is bound by the ALU pipe (LOP3/SHF/IADD3 at 64 lanes/clk/SM)
+    // while the FMA pipe idles; moving the message-schedule additions over is
+    // worth ~4% (tools/sha_variants.cu, profiles/).
+    SNT_HD static uint32_t add_fma(uint32_t a, uint32_t b, uint32_t one) {
+#ifdef __CUDA_ARCH__
+        uint32_t r;
+        asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(one), "r"(b));
+        return r;
+#else
+        return a * one + b;
+#endif
+    }
+
     SNT_HD static void init(uint32_t s[8]) {
         s[0] = 0x6a09e667u; s[1] = 0xbb67ae85u; s[2] = 0x3c6ef372u; s[3] = 0xa54ff53au;
         s[4] = 0x510e527fu; s[5] = 0x9b05688cu; s[6] = 0x1f83d9abu; s[7] = 0x5be0cd19u;
@@ -40,13 +55,15 @@ struct Sha256 {
 
     // One compression. w[16] holds the block as big-endian-decoded words and
     // is overwritten by the rolling schedule.
-    SNT_HD static void compress(uint32_t s[8], uint32_t w[16]) {
+    SNT_HD static void compress(uint32_t s[8], uint32_t w[16], uint32_t one = 1u) {
         const uint32_t K[64] = {SNT_SHA256_K};
         uint32_t a = s[0], b = s[1], c = s[2], d = s[3], e = s[4], f = s[5], g = s[6], h = s[7];
 #pragma unroll
         for (int t = 0; t < 64; ++t) {
             if (t >= 16) {
-                w[t & 15] = w[t & 15] + ssig1(w[(t - 2) & 15]) + w[(t - 7) & 15] + ssig0(w[(t - 15) & 15]);
+                const uint32_t x = add_fma(w[t & 15], w[(t - 7) & 15], one);
+                const uint32_t y = add_fma(ssig1(w[(t - 2) & 15]), ssig0(w[(t - 15) & 15]), one);
+                w[t & 15] = add_fma(x, y, one);
             }
             const uint32_t t1 = h + bsig1(e) + ch(e, f, g) + K[t] + w[t & 15];
             const uint32_t t2 = bsig0(a) + maj(a, b, c);
@@ -91,7 +108,7 @@ struct Sha256 {
     // Whole message at p[0..len), any alignment, any length (generic path).
     // One loop, one compress call site: data blocks first, then the one or
     // two padding blocks (0x80, zeros, 64-bit big-endian bit length).
-    SNT_HD static void hash_message(const uint8_t* p, uint64_t len, uint32_t s[8]) {
+    SNT_HD static void hash_message(const uint8_t* p, uint64_t len, uint32_t s[8], uint32_t one = 1u) {
         init(s);
         const uint64_t nfull = len >> 6;
         const uint32_t rem = static_cast<uint32_t>(len & 63);
@@ -125,7 +142,7 @@ struct Sha256 {
                     w[15] = static_cast<uint32_t>(bits);
                 }
             }
-            compress(s, w);
+            compress(s, w, one);
         }
     }
 
@@ -133,13 +150,13 @@ struct Sha256 {
     // words (= the digest read as big-endian words). 64-byte message: one
     // data compression plus the constant padding block.
     SNT_HD static void hash_pair(const uint32_t l[8], const uint32_t r[8],
-                                 const uint32_t* __restrict__ pad64_kw, uint32_t out[8]) {
+                                 const uint32_t* __restrict__ pad64_kw, uint32_t out[8], uint32_t one = 1u) {
         uint32_t w[16];
 #pragma unroll
         for (int i = 0; i < 8; ++i) { w[i] = l[i]; w[8 + i] = r[i]; }
         uint32_t s[8];
         init(s);
-        compress(s, w);
+        compress(s, w, one);
         compress_const(s, pad64_kw);
 #pragma unroll
         for (int i = 0; i < 8; ++i) out[i] = s[i];

@@ -15,7 +15,10 @@ template <int ALG>
 static void leaf_bytes(const uint8_t* p, uint64_t len, uint8_t* out) {
     using A = AlgTraits<ALG>;
     uint32_t d[A::DW];
-    A::leaf(p, len, d);
+    MerkleConsts c;
+    memset(&c, 0, sizeof(c));
+    c.one = 1;
+    A::leaf(p, len, c, d);
     for (int i = 0; i < A::DW; ++i) {
         const uint32_t w = A::to_mem(d[i]);
         memcpy(out + 4 * i, &w, 4);
@@ -53,6 +56,7 @@ int hc_pair(int alg, const uint8_t* l, const uint8_t* r, uint8_t* out) {
     MerkleConsts c;
     memset(&c, 0, sizeof(c));
     Sha256::pad_schedule(64, c.sha256_pad_node);
+    c.one = 1;
     switch (alg) {
         case ALG_SHA256: pair_bytes<ALG_SHA256>(l, r, c, out); return 0;
         case ALG_BLAKE2B: pair_bytes<ALG_BLAKE2B>(l, r, c, out); return 0;

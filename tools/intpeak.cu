@@ -31,13 +31,19 @@ constexpr int THREADS = 256;
 constexpr int CHAINS = 8;
 constexpr int INNER = 64;      // ops per chain per loop iteration
 
-enum Op { OP_LOP3, OP_SHF, OP_IADD3, OP_PRMT, OP_IMAD, OP_MIX_LOP3_IMAD, OP_MIX_SHF_LOP3_IADD, OP_IMAD_WIDE, OP_MIX_LOP3_WIDE, OP_IMAD_HI };
+enum Op { OP_LOP3, OP_SHF, OP_IADD3, OP_PRMT, OP_IMAD, OP_MIX_LOP3_IMAD, OP_MIX_SHF_LOP3_IADD, OP_IMAD_WIDE, OP_MIX_LOP3_WIDE, OP_IMAD_HI,
+          OP_DEP_LOP3_IMAD, OP_MIX21_DISTINCT, OP_MIX11_DISTINCT, OP_LOP3_DISTINCT, OP_IMAD_DISTINCT, OP_SHF_IMAD_DISTINCT };
 
 template <int OP>
 __global__ void __launch_bounds__(THREADS) op_kernel(uint32_t* out, int iters, uint32_t seed) {
     uint32_t x[CHAINS], y = seed ^ threadIdx.x, z = seed * 2654435761u + blockIdx.x;
+    uint32_t yy[CHAINS], zz[CHAINS];      // per-chain operands: no operand-reuse-cache help
 #pragma unroll
-    for (int c = 0; c < CHAINS; ++c) x[c] = seed + c * 0x9e3779b9u + threadIdx.x;
+    for (int c = 0; c < CHAINS; ++c) {
+        x[c] = seed + c * 0x9e3779b9u + threadIdx.x;
+        yy[c] = (seed ^ threadIdx.x) * (2 * c + 3);
+        zz[c] = seed * 2654435761u + blockIdx.x + c;
+    }
     for (int it = 0; it < iters; ++it) {
 #pragma unroll
         for (int k = 0; k < INNER; ++k) {
@@ -63,6 +69,23 @@ __global__ void __launch_bounds__(THREADS) op_kernel(uint32_t* out, int iters, u
                     if (c & 1) asm volatile("{ .reg .u64 t; .reg .u32 a, b; mul.wide.u32 t, %0, %1; mov.b64 {a, b}, t; add.u32 %0, a, b; }"
                                             : "+r"(x[c]) : "r"(y));
                     else asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(x[c]) : "r"(y), "r"(z));
+                } else if (OP == OP_DEP_LOP3_IMAD) {
+                    // one dependent chain hopping between the pipes: counted as 2 ops
+                    asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(x[c]) : "r"(yy[c]), "r"(zz[c]));
+                    asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(x[c]) : "r"(yy[c]), "r"(zz[c]));
+                } else if (OP == OP_MIX21_DISTINCT) {
+                    if (c % 3 == 2) asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(x[c]) : "r"(yy[c]), "r"(zz[c]));
+                    else asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(x[c]) : "r"(yy[c]), "r"(zz[c]));
+                } else if (OP == OP_MIX11_DISTINCT) {
+                    if (c & 1) asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(x[c]) : "r"(yy[c]), "r"(zz[c]));
+                    else asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(x[c]) : "r"(yy[c]), "r"(zz[c]));
+                } else if (OP == OP_LOP3_DISTINCT) {
+                    asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(x[c]) : "r"(yy[c]), "r"(zz[c]));
+                } else if (OP == OP_IMAD_DISTINCT) {
+                    asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(x[c]) : "r"(yy[c]), "r"(zz[c]));
+                } else if (OP == OP_SHF_IMAD_DISTINCT) {
+                    if (c & 1) asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(x[c]) : "r"(yy[c]), "r"(zz[c]));
+                    else asm volatile("shf.r.wrap.b32 %0, %0, %0, 7;" : "+r"(x[c]));
                 } else if (OP == OP_MIX_LOP3_IMAD) {
                     if (c & 1) asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(x[c]) : "r"(y), "r"(z));
                     else asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(x[c]) : "r"(y), "r"(z));
@@ -77,7 +100,7 @@ __global__ void __launch_bounds__(THREADS) op_kernel(uint32_t* out, int iters, u
     }
     uint32_t r = 0;
 #pragma unroll
-    for (int c = 0; c < CHAINS; ++c) r ^= x[c];
+    for (int c = 0; c < CHAINS; ++c) r ^= x[c] ^ yy[c] ^ zz[c];
     if (r == 0x12345678u) out[blockIdx.x * THREADS + threadIdx.x] = r;
 }
 
@@ -164,6 +187,12 @@ int main() {
     RUN_OP("imad_wide_plus_lop3", OP_IMAD_WIDE, 1.0)
     RUN_OP("imad_hi", OP_IMAD_HI, 1.0)
     RUN_OP("mix_lop3_widepair", OP_MIX_LOP3_WIDE, 1.0)
+    RUN_OP("dep_lop3_imad", OP_DEP_LOP3_IMAD, 2.0)
+    RUN_OP("mix21_distinct", OP_MIX21_DISTINCT, 1.0)
+    RUN_OP("mix11_distinct", OP_MIX11_DISTINCT, 1.0)
+    RUN_OP("lop3_distinct", OP_LOP3_DISTINCT, 1.0)
+    RUN_OP("imad_distinct", OP_IMAD_DISTINCT, 1.0)
+    RUN_OP("shf_imad_distinct", OP_SHF_IMAD_DISTINCT, 1.0)
 
     {
         const int it = 256;

@@ -1,0 +1,199 @@
+// Leaf-kernel experiments for SHA-256 (the dominant kernel of the model path).
+//
+// One big device buffer is cut into 8 KiB leaves; each variant hashes every leaf
+// (one thread per leaf) and is checked against the first variant's digests.
+// Knobs: CTA size, registers (min blocks per SM), schedule adds on the FMA pipe,
+// loads per iteration (64 or 128 bytes per thread), cache hints.
+// Prints one JSON line per variant with GB/s (bytes hashed / kernel time).
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+
+#include "../paper_2510_00554_b200/csrc/sha256.cuh"
+
+using namespace snt;
+
+#define CHECK(x)                                                                      \
+    do {                                                                              \
+        cudaError_t e = (x);                                                          \
+        if (e != cudaSuccess) {                                                       \
+            fprintf(stderr, "%s: %s\n", #x, cudaGetErrorString(e));                   \
+            exit(1);                                                                  \
+        }                                                                             \
+    } while (0)
+
+struct Params {
+    uint32_t pad_kw[64];
+    uint32_t one;
+};
+
+__device__ __forceinline__ U4 ld128_default(const void* p) {
+    U4 r;
+    asm volatile("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+    return r;
+}
+// sm_100a has 256-bit global loads (LDG.256); the L2::evict_first hint is only legal on them.
+// Loads 32 bytes into two U4 halves.
+__device__ __forceinline__ void ld256_evict_first(const void* p, U4& a, U4& b) {
+    asm volatile("ld.global.nc.L1::no_allocate.L2::evict_first.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w) : "l"(p));
+}
+
+template <int HINT>
+__device__ __forceinline__ U4 ldv(const void* p) {
+    if (HINT == 0) return ld128(p);
+    return ld128_default(p);
+}
+
+// 64 bytes: four LDG.128, or two LDG.256 for HINT == 2
+template <int HINT>
+__device__ __forceinline__ void ld64B(const uint8_t* p, U4& q0, U4& q1, U4& q2, U4& q3) {
+    if (HINT == 2) {
+        ld256_evict_first(p, q0, q1);
+        ld256_evict_first(p + 32, q2, q3);
+    } else {
+        q0 = ldv<HINT>(p); q1 = ldv<HINT>(p + 16); q2 = ldv<HINT>(p + 32); q3 = ldv<HINT>(p + 48);
+    }
+}
+
+__device__ __forceinline__ void to_words(const U4& q0, const U4& q1, const U4& q2, const U4& q3, uint32_t w[16]) {
+    w[0] = bswap32(q0.x);  w[1] = bswap32(q0.y);  w[2] = bswap32(q0.z);  w[3] = bswap32(q0.w);
+    w[4] = bswap32(q1.x);  w[5] = bswap32(q1.y);  w[6] = bswap32(q1.z);  w[7] = bswap32(q1.w);
+    w[8] = bswap32(q2.x);  w[9] = bswap32(q2.y);  w[10] = bswap32(q2.z); w[11] = bswap32(q2.w);
+    w[12] = bswap32(q3.x); w[13] = bswap32(q3.y); w[14] = bswap32(q3.z); w[15] = bswap32(q3.w);
+}
+
+// THREADS per CTA, MINB = min CTAs per SM (register cap), IMAD = schedule adds on FMA pipe,
+// WIDE = 128 bytes per thread per iteration, HINT = load flavour
+template <int THREADS, int MINB, int IMAD, int WIDE, int HINT>
+__global__ void __launch_bounds__(THREADS, MINB)
+leaf_kernel(const uint8_t* __restrict__ data, uint64_t n_leaves, const __grid_constant__ Params prm,
+            uint8_t* __restrict__ out) {
+    const uint64_t k = static_cast<uint64_t>(blockIdx.x) * THREADS + threadIdx.x;
+    if (k >= n_leaves) return;
+    const uint8_t* p = data + (k << 13);
+    const uint32_t one = IMAD ? prm.one : 1u;
+    uint32_t s[8];
+    Sha256::init(s);
+    if (!WIDE) {
+        U4 q0, q1, q2, q3;
+        ld64B<HINT>(p, q0, q1, q2, q3);
+#pragma unroll 1
+        for (uint32_t b = 0; b < 128; ++b) {
+            uint32_t w[16];
+            to_words(q0, q1, q2, q3, w);
+            if (b + 1 < 128) {
+                ld64B<HINT>(p + ((b + 1) << 6), q0, q1, q2, q3);
+            }
+            Sha256::compress(s, w, one);
+        }
+    } else {
+        U4 q[8];
+        ld64B<HINT>(p, q[0], q[1], q[2], q[3]);
+        ld64B<HINT>(p + 64, q[4], q[5], q[6], q[7]);
+#pragma unroll 1
+        for (uint32_t b = 0; b < 64; ++b) {
+            uint32_t w[16], w2[16];
+            to_words(q[0], q[1], q[2], q[3], w);
+            to_words(q[4], q[5], q[6], q[7], w2);
+            if (b + 1 < 64) {
+                const uint8_t* n = p + ((b + 1) << 7);
+                ld64B<HINT>(n, q[0], q[1], q[2], q[3]);
+                ld64B<HINT>(n + 64, q[4], q[5], q[6], q[7]);
+            }
+            Sha256::compress(s, w, one);
+            Sha256::compress(s, w2, one);
+        }
+    }
+    Sha256::compress_const(s, prm.pad_kw);
+    uint4* o = reinterpret_cast<uint4*>(out + k * 32);
+    o[0] = make_uint4(bswap32(s[0]), bswap32(s[1]), bswap32(s[2]), bswap32(s[3]));
+    o[1] = make_uint4(bswap32(s[4]), bswap32(s[5]), bswap32(s[6]), bswap32(s[7]));
+}
+
+static uint8_t* g_data;
+static uint8_t* g_out;
+static uint8_t* g_ref;
+static uint64_t g_leaves;
+static Params g_prm;
+static std::vector<uint8_t> h_ref, h_out;
+
+template <int THREADS, int MINB, int IMAD, int WIDE, int HINT>
+static void run(const char* name, bool is_ref = false) {
+    const unsigned grid = static_cast<unsigned>((g_leaves + THREADS - 1) / THREADS);
+    cudaFuncAttributes attr;
+    CHECK(cudaFuncGetAttributes(&attr, leaf_kernel<THREADS, MINB, IMAD, WIDE, HINT>));
+    CHECK(cudaMemset(g_out, 0, g_leaves * 32));
+    leaf_kernel<THREADS, MINB, IMAD, WIDE, HINT><<<grid, THREADS>>>(g_data, g_leaves, g_prm, is_ref ? g_ref : g_out);
+    CHECK(cudaDeviceSynchronize());
+    int ok = 1;
+    if (is_ref) {
+        CHECK(cudaMemcpy(h_ref.data(), g_ref, g_leaves * 32, cudaMemcpyDeviceToHost));
+    } else {
+        CHECK(cudaMemcpy(h_out.data(), g_out, g_leaves * 32, cudaMemcpyDeviceToHost));
+        ok = memcmp(h_out.data(), h_ref.data(), g_leaves * 32) == 0;
+    }
+    cudaEvent_t e0, e1;
+    CHECK(cudaEventCreate(&e0));
+    CHECK(cudaEventCreate(&e1));
+    float best = 1e30f, sum = 0;
+    const int reps = 5;
+    for (int r = 0; r < reps; ++r) {
+        CHECK(cudaEventRecord(e0));
+        leaf_kernel<THREADS, MINB, IMAD, WIDE, HINT><<<grid, THREADS>>>(g_data, g_leaves, g_prm, g_out);
+        CHECK(cudaEventRecord(e1));
+        CHECK(cudaEventSynchronize(e1));
+        float ms;
+        CHECK(cudaEventElapsedTime(&ms, e0, e1));
+        best = ms < best ? ms : best;
+        sum += ms;
+    }
+    CHECK(cudaGetLastError());
+    const double bytes = double(g_leaves) * 8192;
+    printf("{\"variant\": \"%s\", \"threads\": %d, \"minb\": %d, \"imad\": %d, \"wide\": %d, \"hint\": %d, \"regs\": %d, "
+           "\"ok\": %d, \"best_ms\": %.4f, \"avg_ms\": %.4f, \"gbs_best\": %.1f}\n",
+           name, THREADS, MINB, IMAD, WIDE, HINT, attr.numRegs, ok, best, sum / reps, bytes / (best * 1e-3) / 1e9);
+    fflush(stdout);
+}
+
+int main(int argc, char** argv) {
+    g_leaves = argc > 1 ? strtoull(argv[1], nullptr, 10) : 799954ull;
+    CHECK(cudaMalloc(&g_data, g_leaves * 8192));
+    CHECK(cudaMalloc(&g_out, g_leaves * 32));
+    CHECK(cudaMalloc(&g_ref, g_leaves * 32));
+    h_ref.resize(g_leaves * 32);
+    h_out.resize(g_leaves * 32);
+    // pseudo-random fill on the host in 64 MiB pieces
+    {
+        std::vector<uint32_t> buf(16u << 20);
+        uint32_t x = 12345;
+        for (uint64_t off = 0; off < g_leaves * 8192; off += buf.size() * 4) {
+            for (auto& v : buf) { x = x * 1664525u + 1013904223u; v = x; }
+            uint64_t n = g_leaves * 8192 - off;
+            if (n > buf.size() * 4) n = buf.size() * 4;
+            CHECK(cudaMemcpy(g_data + off, buf.data(), n, cudaMemcpyHostToDevice));
+        }
+    }
+    Sha256::pad_schedule(8192, g_prm.pad_kw);
+    g_prm.one = 1;
+
+    run<128, 1, 0, 0, 0>("ref", true);
+    run<128, 1, 0, 0, 0>("t128");
+    run<128, 1, 1, 0, 0>("t128+imad");
+    run<64, 1, 0, 0, 0>("t64");
+    run<64, 1, 1, 0, 0>("t64+imad");
+    run<256, 1, 0, 0, 0>("t256");
+    run<256, 1, 1, 0, 0>("t256+imad");
+    run<128, 10, 0, 0, 0>("t128 minb10 (<=48 regs)");
+    run<128, 10, 1, 0, 0>("t128 minb10+imad");
+    run<128, 12, 1, 0, 0>("t128 minb12+imad (<=40 regs)");
+    run<128, 1, 0, 1, 0>("t128 wide");
+    run<128, 1, 1, 1, 0>("t128 wide+imad");
+    run<128, 1, 1, 0, 1>("t128+imad ld.nc default");
+    run<128, 1, 1, 0, 2>("t128+imad ldg256 evict_first");
+    run<128, 1, 1, 1, 2>("t128 wide+imad ldg256 evict_first");
+    return 0;
+}
