@@ -46,6 +46,9 @@ const char* snt_last_cuda_error(void);
 uint32_t snt_abi_version(void);
 /* Diagnostic: kernels launched by this library in this process so far. */
 uint64_t snt_debug_launch_count(void);
+/* Diagnostic/test knob for the LtHash kernels: 0 = choose by item count (default),
+ * 1 = one thread per item, 2 = four lanes per item. Results are identical. */
+void snt_debug_lthash_mode(int mode);
 /* 32, 64, 32 -- or 0 for an unknown algorithm. */
 uint32_t snt_digest_len(int alg);
 
@@ -54,12 +57,16 @@ uint32_t snt_digest_len(int alg);
  * (address, byte length, first leaf index) kept on the device, searched by
  * the kernels. Empty tensors own no leaves; the last leaf of a tensor is
  * hashed at its true length. Creating a plan allocates one small device
- * buffer and synchronises once; hashing calls never allocate.
+ * buffer with the stream-ordered allocator and fills it with an asynchronous
+ * copy on `stream`; use the plan on that stream (or order other streams after
+ * it). Destroying it frees the buffer in stream order. Hashing calls never
+ * allocate and nothing here synchronises the device.
  */
 typedef struct snt_model_plan snt_model_plan;
 
 int snt_model_plan_create(const void* const* d_tensor_ptrs, const uint64_t* tensor_nbytes,
-                          uint32_t n_tensors, uint32_t block_size, snt_model_plan** out_plan);
+                          uint32_t n_tensors, uint32_t block_size, snt_stream_t stream,
+                          snt_model_plan** out_plan);
 void snt_model_plan_destroy(snt_model_plan* plan);
 uint64_t snt_model_plan_leaf_count(const snt_model_plan* plan);
 uint64_t snt_model_plan_total_bytes(const snt_model_plan* plan);

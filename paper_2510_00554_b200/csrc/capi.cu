@@ -61,7 +61,10 @@ const MerkleConsts& node_consts() {
 }  // namespace
 
 struct snt_model_plan {
-    uint64_t* d_table = nullptr;     // addr[n] | nbytes[n] | first_leaf[n + 1]
+    uint64_t* d_table = nullptr;     // addr[n] | nbytes[n] | first_leaf[n + 1] | irregular[n_irregular]
+    uint32_t n_irregular = 0;        // leaves that are ragged or not 16-byte aligned (SHA-256 generic path)
+    cudaStream_t stream = nullptr;   // the stream the table was allocated and filled on
+    std::vector<uint64_t> host;      // staging copy of the table (kept alive until destroy)
     uint32_t n_tensors = 0;
     uint32_t block_shift = 0;
     uint64_t n_leaves = 0;
@@ -109,7 +112,8 @@ uint32_t snt_digest_len(int alg) {
 }
 
 int snt_model_plan_create(const void* const* d_tensor_ptrs, const uint64_t* tensor_nbytes,
-                          uint32_t n_tensors, uint32_t block_size, snt_model_plan** out_plan) {
+                          uint32_t n_tensors, uint32_t block_size, snt_stream_t stream,
+                          snt_model_plan** out_plan) {
     if (!out_plan) return SNT_ERR_INVALID_INPUT;
     *out_plan = nullptr;
     if (block_size < 64 || (block_size & (block_size - 1))) return SNT_ERR_CONFIG;   // model.py:94-95
@@ -117,16 +121,27 @@ int snt_model_plan_create(const void* const* d_tensor_ptrs, const uint64_t* tens
     uint32_t shift = 0;
     while ((1u << shift) < block_size) ++shift;
     std::vector<uint64_t> host(3ull * n_tensors + 1);
+    std::vector<uint64_t> irregular;
     uint64_t leaves = 0, total = 0;
     for (uint32_t t = 0; t < n_tensors; ++t) {
-        host[t] = reinterpret_cast<uint64_t>(d_tensor_ptrs[t]);
-        host[n_tensors + t] = tensor_nbytes[t];
+        const uint64_t addr = reinterpret_cast<uint64_t>(d_tensor_ptrs[t]);
+        const uint64_t nb = tensor_nbytes[t];
+        host[t] = addr;
+        host[n_tensors + t] = nb;
         host[2ull * n_tensors + t] = leaves;
-        leaves += (tensor_nbytes[t] + block_size - 1) >> shift;
-        total += tensor_nbytes[t];
-        if (tensor_nbytes[t] && !d_tensor_ptrs[t]) return SNT_ERR_INVALID_INPUT;
+        const uint64_t count = (nb + block_size - 1) >> shift;
+        if (nb && !d_tensor_ptrs[t]) return SNT_ERR_INVALID_INPUT;
+        if (addr & 15) {
+            for (uint64_t j = 0; j < count; ++j) irregular.push_back(leaves + j);
+        } else if (nb & (block_size - 1)) {
+            irregular.push_back(leaves + count - 1);
+        }
+        leaves += count;
+        total += nb;
     }
+    if (irregular.size() > 0xffffffffull) return SNT_ERR_INVALID_INPUT;
     host[3ull * n_tensors] = leaves;
+    host.insert(host.end(), irregular.begin(), irregular.end());
     if (total == 0) return SNT_ERR_INVALID_INPUT;                                     // model.py:166-168
     snt_model_plan* p = new (std::nothrow) snt_model_plan();
     if (!p) return SNT_ERR_RESOURCE;
@@ -134,13 +149,18 @@ int snt_model_plan_create(const void* const* d_tensor_ptrs, const uint64_t* tens
     p->block_shift = shift;
     p->n_leaves = leaves;
     p->total_bytes = total;
+    p->n_irregular = static_cast<uint32_t>(irregular.size());
     p->consts = node_consts();
     Sha256::pad_schedule(block_size, p->consts.sha256_pad_leaf);
-    cudaError_t e = cudaMalloc(&p->d_table, host.size() * sizeof(uint64_t));
+    // stream-ordered allocation and copy: no device-wide synchronisation on the hashing path
+    p->stream = static_cast<cudaStream_t>(stream);
+    p->host.swap(host);
+    const size_t bytes = p->host.size() * sizeof(uint64_t);
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&p->d_table), bytes, p->stream);
     if (e == cudaSuccess)
-        e = cudaMemcpy(p->d_table, host.data(), host.size() * sizeof(uint64_t), cudaMemcpyHostToDevice);
+        e = cudaMemcpyAsync(p->d_table, p->host.data(), bytes, cudaMemcpyHostToDevice, p->stream);
     if (e != cudaSuccess) {
-        if (p->d_table) cudaFree(p->d_table);
+        if (p->d_table) cudaFreeAsync(p->d_table, p->stream);
         delete p;
         return cuda_fail(e, "snt_model_plan_create");
     }
@@ -150,7 +170,7 @@ int snt_model_plan_create(const void* const* d_tensor_ptrs, const uint64_t* tens
 
 void snt_model_plan_destroy(snt_model_plan* plan) {
     if (!plan) return;
-    if (plan->d_table) cudaFree(plan->d_table);
+    if (plan->d_table) cudaFreeAsync(plan->d_table, plan->stream);   // ordered after the launches on that stream
     delete plan;
 }
 
@@ -223,10 +243,12 @@ template <int ALG>
 int launch_leaves(const snt_model_plan* plan, uint64_t begin, uint64_t end, uint8_t* d_leaves,
                   cudaStream_t s) {
     const uint64_t n = end - begin;
-    const uint64_t grid = (n + LEAF_THREADS - 1) / LEAF_THREADS;
+    const uint32_t irr_ctas = ALG == ALG_SHA256 ? (plan->n_irregular + LEAF_THREADS - 1) / LEAF_THREADS : 0;
+    const uint64_t grid = (n + LEAF_THREADS - 1) / LEAF_THREADS + irr_ctas;
     if (grid > 0x7fffffffull) return SNT_ERR_INVALID_INPUT;
+    const uint64_t* irregular = plan->d_table + 3ull * plan->n_tensors + 1;
     merkle_leaf_kernel<ALG><<<static_cast<unsigned>(grid), LEAF_THREADS, 0, s>>>(
-        plan->table(), plan->consts, begin, end, d_leaves);
+        plan->table(), plan->consts, begin, end, irregular, plan->n_irregular, irr_ctas, d_leaves);
     SNT_CUDA(cudaGetLastError());
     ++g_launches;
     return SNT_OK;
@@ -243,21 +265,42 @@ int launch_blocks(const uint8_t* base, const uint64_t* off, const uint64_t* len,
     return SNT_OK;
 }
 
+// Item counts below this would use four lanes per item (lthash_quad_kernel). Measured on B200
+// (CIFAR-shaped 50k x 3 KiB: 0.277 ms quad vs 0.216 ms one thread per item; profiles/) the quad
+// form loses: its G functions have no instruction-level parallelism left and every round adds
+// 12 shuffles. It stays selectable through snt_debug_lthash_mode for experiments and tests.
+constexpr uint64_t LT_QUAD_MAX_ITEMS = 0;
+std::atomic<int> g_lthash_mode{0};       // debug knob: 0 auto, 1 one thread per item, 2 quad
+
 template <class Items>
 int launch_lthash(const Items& items, uint64_t n, uint32_t n_sources, uint32_t* d_acc,
                   uint64_t* d_counts, void* d_digests, uint32_t* d_status, cudaStream_t s) {
     if (n == 0) return SNT_OK;
-    const uint64_t grid = (n + LT_THREADS - 1) / LT_THREADS;
-    if (grid > 0x7fffffffull) return SNT_ERR_INVALID_INPUT;
     auto* counts = reinterpret_cast<unsigned long long*>(d_counts);
     auto* dig = static_cast<uint8_t*>(d_digests);
-    if (n_sources <= static_cast<uint32_t>(LT_SMEM_SOURCES)) {
-        const size_t smem = static_cast<size_t>(n_sources) * (LT_LANES + 1) * sizeof(uint32_t);
-        lthash_kernel<Items, true><<<static_cast<unsigned>(grid), LT_THREADS, smem, s>>>(
-            items, n, n_sources, d_acc, counts, dig, d_status);
+    const bool smem_acc = n_sources <= static_cast<uint32_t>(LT_SMEM_SOURCES);
+    const size_t acc_bytes = smem_acc ? static_cast<size_t>(n_sources) * (LT_LANES + 1) * sizeof(uint32_t) : 0;
+    const int mode = g_lthash_mode.load();
+    const bool quad = mode == 2 || (mode == 0 && n < LT_QUAD_MAX_ITEMS);   // LT_QUAD_MAX_ITEMS == 0: never by default
+    if (quad) {
+        const uint64_t grid = (n + LTQ_QUADS - 1) / LTQ_QUADS;
+        if (grid > 0x7fffffffull) return SNT_ERR_INVALID_INPUT;
+        const size_t smem = static_cast<size_t>(LTQ_QUADS) * QUAD_REGION_BYTES + acc_bytes;
+        if (smem_acc)
+            lthash_quad_kernel<Items, true><<<static_cast<unsigned>(grid), LTQ_THREADS, smem, s>>>(
+                items, n, n_sources, d_acc, counts, dig, d_status);
+        else
+            lthash_quad_kernel<Items, false><<<static_cast<unsigned>(grid), LTQ_THREADS, smem, s>>>(
+                items, n, n_sources, d_acc, counts, dig, d_status);
     } else {
-        lthash_kernel<Items, false><<<static_cast<unsigned>(grid), LT_THREADS, 0, s>>>(
-            items, n, n_sources, d_acc, counts, dig, d_status);
+        const uint64_t grid = (n + LT_THREADS - 1) / LT_THREADS;
+        if (grid > 0x7fffffffull) return SNT_ERR_INVALID_INPUT;
+        if (smem_acc)
+            lthash_kernel<Items, true><<<static_cast<unsigned>(grid), LT_THREADS, acc_bytes, s>>>(
+                items, n, n_sources, d_acc, counts, dig, d_status);
+        else
+            lthash_kernel<Items, false><<<static_cast<unsigned>(grid), LT_THREADS, 0, s>>>(
+                items, n, n_sources, d_acc, counts, dig, d_status);
     }
     SNT_CUDA(cudaGetLastError());
     ++g_launches;
@@ -267,6 +310,8 @@ int launch_lthash(const Items& items, uint64_t n, uint32_t n_sources, uint32_t* 
 }  // namespace
 
 extern "C" {
+
+void snt_debug_lthash_mode(int mode) { g_lthash_mode.store(mode); }
 
 int snt_merkle_leaves(const snt_model_plan* plan, int alg, uint64_t leaf_begin, uint64_t leaf_end,
                       void* d_leaves, snt_stream_t stream) {

@@ -65,28 +65,47 @@ SNT_D void load_digest(const uint8_t* in, uint32_t* d) {
 
 // One thread per leaf of [leaf_begin, leaf_end); digest k is written at
 // d_leaves + (k - leaf_begin) * DIGEST_BYTES.
+//
+// SHA-256 splits the leaves in two classes at plan time. "Regular" leaves (full
+// block, 16-byte aligned -- all but a few hundred of them) take the fast path in
+// the main part of the grid; a warp's irregular lanes simply sit that launch
+// out, so one ragged leaf no longer drags its 31 neighbours through the generic
+// path. The irregular leaves (ragged tensor tails, tensors at odd addresses)
+// are listed in `irregular` and hashed by the first `irr_ctas` CTAs of the same
+// grid with the generic path, concurrently with the rest.
 template <int ALG>
 __global__ void __launch_bounds__(LEAF_THREADS)
 merkle_leaf_kernel(const TensorTable tab, const __grid_constant__ MerkleConsts c,
-                   uint64_t leaf_begin, uint64_t leaf_end, uint8_t* __restrict__ d_leaves) {
+                   uint64_t leaf_begin, uint64_t leaf_end, const uint64_t* __restrict__ irregular,
+                   uint32_t n_irregular, uint32_t irr_ctas, uint8_t* __restrict__ d_leaves) {
     using A = AlgTraits<ALG>;
-    const uint64_t k = leaf_begin + static_cast<uint64_t>(blockIdx.x) * LEAF_THREADS + threadIdx.x;
-    const bool exists = k < leaf_end;
-    LeafRef leaf{nullptr, 0};
-    if (exists) leaf = locate_leaf(tab, k);
     uint32_t d[A::DW];
     if (ALG == ALG_SHA256) {
-        const bool fast = exists && leaf.len == (1ull << tab.block_shift) &&
-                          (reinterpret_cast<uintptr_t>(leaf.ptr) & 15) == 0;
-        if (__all_sync(0xffffffffu, fast)) {
-            sha256_leaf_aligned(leaf.ptr, 1u << (tab.block_shift - 6), c.sha256_pad_leaf, d, c.one);
-        } else if (exists) {
+        if (blockIdx.x < irr_ctas) {
+            const uint32_t j = blockIdx.x * LEAF_THREADS + threadIdx.x;
+            if (j >= n_irregular) return;
+            const uint64_t k = irregular[j];
+            if (k < leaf_begin || k >= leaf_end) return;
+            const LeafRef leaf = locate_leaf(tab, k);
             A::leaf(leaf.ptr, leaf.len, c, d);
+            store_digest<ALG>(d_leaves + (k - leaf_begin) * A::DIGEST_BYTES, d);
+            return;
         }
+        const uint64_t k = leaf_begin + static_cast<uint64_t>(blockIdx.x - irr_ctas) * LEAF_THREADS + threadIdx.x;
+        if (k >= leaf_end) return;
+        const LeafRef leaf = locate_leaf(tab, k);
+        const bool regular = leaf.len == (1ull << tab.block_shift) &&
+                             (reinterpret_cast<uintptr_t>(leaf.ptr) & 15) == 0;
+        if (!regular) return;                              // hashed by the irregular CTAs
+        sha256_leaf_aligned(leaf.ptr, 1u << (tab.block_shift - 6), c.sha256_pad_leaf, d, c.one);
+        store_digest<ALG>(d_leaves + (k - leaf_begin) * A::DIGEST_BYTES, d);
     } else {
-        if (exists) A::leaf(leaf.ptr, leaf.len, c, d);
+        const uint64_t k = leaf_begin + static_cast<uint64_t>(blockIdx.x) * LEAF_THREADS + threadIdx.x;
+        if (k >= leaf_end) return;
+        const LeafRef leaf = locate_leaf(tab, k);
+        A::leaf(leaf.ptr, leaf.len, c, d);
+        store_digest<ALG>(d_leaves + (k - leaf_begin) * A::DIGEST_BYTES, d);
     }
-    if (exists) store_digest<ALG>(d_leaves + (k - leaf_begin) * A::DIGEST_BYTES, d);
 }
 
 // hash_blocks over an explicit (address, length) list: entry i = H(block i)

@@ -95,7 +95,7 @@ class ModelPlan:
             nbytes = t.numel() if sizes_override is None else int(sizes_override[i])
             ptrs[i] = t.data_ptr() if nbytes else None
             sizes[i] = nbytes
-        rc = lib.snt_model_plan_create(ptrs, sizes, n, block_size, ctypes.byref(self._handle))
+        rc = lib.snt_model_plan_create(ptrs, sizes, n, block_size, _stream(), ctypes.byref(self._handle))
         _native.check(rc, "snt_model_plan_create")
         self.block_size = block_size
         self.leaf_count = int(lib.snt_model_plan_leaf_count(self._handle))
@@ -161,12 +161,23 @@ class MerkleModelHasher:
                                     _ptr(self.out), _stream())
         _native.check(rc, "snt_merkle_inplace")
 
-    def run_leaves_only(self) -> None:
-        """The leaf stage alone (``snt_merkle_leaves``); used to time the dominant kernel."""
+    def run_leaves_only(self, begin: Optional[int] = None, end: Optional[int] = None) -> None:
+        """The leaf stage alone (``snt_merkle_leaves``) over [begin, end) of this hasher's range."""
         lib = _native.load()
-        rc = lib.snt_merkle_leaves(self.plan.handle, ALG_IDS[self.alg], self.leaf_begin, self.leaf_end,
-                                   _ptr(self.leaves), _stream())
+        begin = self.leaf_begin if begin is None else begin
+        end = self.leaf_end if end is None else end
+        out = self.leaves[(begin - self.leaf_begin) * self.dlen:]
+        rc = lib.snt_merkle_leaves(self.plan.handle, ALG_IDS[self.alg], begin, end, _ptr(out), _stream())
         _native.check(rc, "snt_merkle_leaves")
+
+    def run_tree_only(self) -> None:
+        """Reduce the leaf digests already in ``self.leaves`` to the root (whole-model hashers only)."""
+        if self.levels is not None or self.leaf_begin != 0 or self.leaf_end != self.plan.leaf_count:
+            raise InvalidInput("run_tree_only needs a whole-model hasher")
+        lib = _native.load()
+        rc = lib.snt_merkle_root(ALG_IDS[self.alg], _ptr(self.leaves), self.plan.leaf_count, _ptr(self.work),
+                                 self.work_bytes, _ptr(self.out), _stream())
+        _native.check(rc, "snt_merkle_root")
 
     def out_bytes(self) -> bytes:
         return self.out.cpu().numpy().tobytes()

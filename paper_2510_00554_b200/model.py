@@ -194,9 +194,83 @@ def _hash_plan(cfg: HashConfig, plan: _dev.ModelPlan, aux_data_bytes: int = 0) -
                              aux_digest_bytes=acc.acc.numel() * 4)
 
 
+STAGE_PIPELINE_MIN_BYTES = 32 << 20     # host inputs above this are copied and hashed in overlapped chunks
+STAGE_CHUNK_BYTES = 256 << 20
+
+
+def _is_cuda(buf) -> bool:
+    return isinstance(buf, torch.Tensor) and buf.device.type == "cuda"
+
+
+def _host_tensor(buf) -> torch.Tensor:
+    """Flat uint8 CPU tensor over a host buffer (zero copy; pinned tensors stay pinned)."""
+    if isinstance(buf, torch.Tensor):
+        t = buf.detach()
+        t = t if t.is_contiguous() else t.contiguous()
+        t = t.reshape(-1)
+        return t if t.dtype == torch.uint8 else t.view(torch.uint8)
+    import warnings
+
+    arr = _dev.host_bytes_view(buf)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        return torch.from_numpy(arr)
+
+
+def _inplace_merkle_staged(cfg: HashConfig, model: TensorMap) -> ModelDigestResult:
+    """Host tensors -> device with the copies and the leaf hashing overlapped.
+
+    Device buffers are allocated up front (the plan needs their addresses); the
+    copies run on a side stream in ~256 MB groups of whole tensors and the leaf
+    kernel for a group is enqueued as soon as its bytes have landed. The tree
+    reduction runs once at the end over the leaf digests.
+    """
+    dev = _dev.require_cuda()
+    bs = cfg.block_size
+    sizes = [buffer_nbytes(buf) for _, buf in model.entries]
+    dst: List[torch.Tensor] = []
+    for (_, buf), nbytes in zip(model.entries, sizes):
+        dst.append(_dev.as_device_bytes(buf, dev) if _is_cuda(buf) else
+                   torch.empty(nbytes, dtype=torch.uint8, device=dev))
+    plan = _dev.ModelPlan(dst, bs)
+    try:
+        hasher = _dev.MerkleModelHasher(plan, cfg.alg.value)
+        main = torch.cuda.current_stream()
+        side = torch.cuda.Stream()
+        side.wait_stream(main)
+        first, group_begin, group_bytes, pending = 0, 0, 0, []
+        n = len(dst)
+        for i, (_, buf) in enumerate(model.entries):
+            if not _is_cuda(buf) and sizes[i]:
+                pending.append(i)
+            group_bytes += sizes[i]
+            first_next = first + -(-sizes[i] // bs)
+            if group_bytes >= STAGE_CHUNK_BYTES or i == n - 1:
+                with torch.cuda.stream(side):
+                    for j in pending:
+                        dst[j].copy_(_host_tensor(model.entries[j][1]), non_blocking=True)
+                    done = torch.cuda.Event()
+                    done.record(side)
+                main.wait_event(done)
+                if first_next > group_begin:
+                    hasher.run_leaves_only(group_begin, first_next)
+                group_begin, group_bytes, pending = first_next, 0, []
+            first = first_next
+        hasher.run_tree_only()
+        root = Digest(cfg.alg, hasher.out_bytes())          # synchronises: all copies and kernels done
+        n_leaves = plan.leaf_count
+        aux = hasher.leaves.numel() + hasher.work_bytes + (hasher.out.numel() if n_leaves > 1 else 0)
+        return ModelDigestResult(root, cfg, n_leaves, aux_digest_bytes=aux)
+    finally:
+        plan.close()
+
+
 def inplace_hash(cfg: HashConfig, model: TensorMap, workers: int = 1) -> ModelDigestResult:
     """Hash fragmented tensors where they lie: no copy, no padding (model.py:298-315)."""
     _require_nonempty(model)
+    host_bytes = sum(buffer_nbytes(buf) for _, buf in model.entries if not _is_cuda(buf))
+    if cfg.construction is Construction.MERKLE and host_bytes >= STAGE_PIPELINE_MIN_BYTES:
+        return _inplace_merkle_staged(cfg, model)
     plan = _dev.ModelPlan(device_tensors(model), cfg.block_size)
     try:
         return _hash_plan(cfg, plan)

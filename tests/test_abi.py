@@ -58,10 +58,10 @@ def test_argument_validation_before_any_cuda_call(lib):
     ptrs = (ctypes.c_void_p * 1)(0x1000)
     sizes = (ctypes.c_uint64 * 1)(100)
     for bad_bs in (0, 63, 100, 8191):                        # model.py:93-95 -> ConfigError
-        assert lib.snt_model_plan_create(ptrs, sizes, 1, bad_bs, ctypes.byref(handle)) == -3
-    assert lib.snt_model_plan_create(ptrs, sizes, 0, 8192, ctypes.byref(handle)) == -1    # no tensors
+        assert lib.snt_model_plan_create(ptrs, sizes, 1, bad_bs, None, ctypes.byref(handle)) == -3
+    assert lib.snt_model_plan_create(ptrs, sizes, 0, 8192, None, ctypes.byref(handle)) == -1    # no tensors
     sizes[0] = 0
-    assert lib.snt_model_plan_create(ptrs, sizes, 1, 8192, ctypes.byref(handle)) == -1    # zero bytes (model.py:166)
+    assert lib.snt_model_plan_create(ptrs, sizes, 1, 8192, None, ctypes.byref(handle)) == -1    # zero bytes (model.py:166)
     assert not handle.value
     assert lib.snt_hash_blocks(0, None, None, None, 0, None, None) == -1                  # merkle.py:100-101
     assert lib.snt_hash_blocks(7, None, None, None, 1, None, None) == -3

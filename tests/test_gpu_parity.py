@@ -189,6 +189,31 @@ def test_unaligned_device_tensors_hashed_in_place(pkg, porc):
     assert pkg.hash_model(cfg, pkg.TensorMap(entries)).model_digest.data == porc.inplace_lattice(host, 1024)
 
 
+def test_host_model_staged_in_overlapped_chunks(pkg, corc, monkeypatch):
+    """Large host models take the copy/hash pipeline: same root, with CUDA entries mixed in."""
+    from paper_2510_00554_b200 import model as mm
+
+    monkeypatch.setattr(mm, "STAGE_CHUNK_BYTES", 3 << 20)          # several chunks at test size
+    rng = np.random.default_rng(11)
+    sizes = [5 << 20, 100, 0, (7 << 20) + 13, 8192, 3, (9 << 20) + 4096, 12 << 20, 6400, (2 << 20) + 1]
+    host = [rng.integers(0, 256, size=s, dtype=np.uint8) for s in sizes]
+    entries = []
+    for i, h in enumerate(host):
+        if i in (3, 8):
+            entries.append((f"t{i}", torch.from_numpy(h).cuda()))          # already resident
+        elif i % 2:
+            entries.append((f"t{i}", torch.from_numpy(h).pin_memory()))    # pinned host tensor
+        else:
+            entries.append((f"t{i}", h.tobytes()))                         # plain bytes
+    assert sum(sizes) >= mm.STAGE_PIPELINE_MIN_BYTES
+    tl = corc.TensorList(host)
+    for name in ALGS:
+        cfg = pkg.HashConfig(pkg.Construction.MERKLE, pkg.Strategy.IN_PLACE, _alg(pkg, name), 8192)
+        res = pkg.hash_model(cfg, pkg.TensorMap(entries))
+        assert res.model_digest.data == corc.inplace_merkle(name, tl, 8192, 4), name
+        assert res.block_count == tl.leaf_count(8192)
+
+
 def test_empty_model_and_bad_config(pkg):
     cfg = pkg.HashConfig(pkg.Construction.MERKLE, pkg.Strategy.IN_PLACE)
     with pytest.raises(pkg.errors.InvalidInput):
@@ -377,6 +402,46 @@ def test_many_sources_take_the_global_accumulator_path(pkg, corc):
     out, counts, _ = acc.digests()
     want_sums, want_counts = corc.lthash_samples(shard, offs, lens, ids, src.astype(np.uint32), n_src, 2)
     assert out == want_sums and counts == want_counts
+
+
+@pytest.mark.parametrize("mode", [1, 2])
+def test_lthash_kernel_variants_agree_with_oracle(pkg, corc, mode):
+    """One thread per item (mode 1) and four lanes per item (mode 2): ragged, unaligned, empty samples."""
+    from paper_2510_00554_b200 import _native
+    from paper_2510_00554_b200 import dataset as ds
+    from paper_2510_00554_b200 import device as dev
+
+    lib = _native.load()
+    n, n_src = 2500, 7
+    rng = np.random.default_rng(40 + mode)
+    lens = rng.choice([0, 1, 7, 8, 9, 119, 120, 121, 127, 128, 129, 247, 248, 249, 256, 1000, 3072], size=n).astype(np.uint64)
+    lens[:200] = rng.integers(0, 5000, size=200)
+    gaps = rng.integers(0, 5, size=n).astype(np.uint64)            # every byte alignment
+    offs = np.zeros(n, dtype=np.uint64)
+    np.cumsum((lens + gaps)[:-1], out=offs[1:])
+    offs += 3
+    shard = rng.integers(0, 256, size=int(offs[-1] + lens[-1]) + 64, dtype=np.uint8)
+    src = rng.integers(0, n_src, size=n)
+    ids = rng.integers(0, 2**63, size=n).astype(np.uint64)
+    want_sums, want_counts, want_digests = corc.lthash_samples(shard, offs, lens, ids, src.astype(np.uint32), n_src, 4,
+                                                               want_digests=True)
+    lib.snt_debug_lthash_mode(mode)
+    try:
+        dset = ds.DeviceDataset.from_host(shard, offs, lens, ids, src, list(range(n_src)))
+        acc = dev.LatticeAccumulator(n_src)
+        per_sample = torch.empty(n * 64, dtype=torch.uint8, device="cuda")
+        dset.accumulate(acc, digests=per_sample)
+        out, counts, status = acc.digests()
+        # the model lattice path (leaf items) through the same kernel variant
+        tensors = inputs.model_tensors(17, [40000, 123, 8192 * 3, 9999, 1, 2, 70001])
+        cfg = pkg.HashConfig(pkg.Construction.LATTICE, pkg.Strategy.IN_PLACE, pkg.CompressionAlg.BLAKE2B, 1024)
+        got_model = pkg.hash_model(cfg, pkg.TensorMap([(f"t{i}", t) for i, t in enumerate(tensors)])).model_digest.data
+    finally:
+        lib.snt_debug_lthash_mode(0)
+    assert status == 0
+    assert per_sample.cpu().numpy().tobytes() == want_digests
+    assert out == want_sums and counts == want_counts
+    assert got_model == corc.inplace_lattice(corc.TensorList(tensors), 1024, 2)
 
 
 def test_sign_and_verify_gpu_digests_end_to_end(pkg):
