@@ -201,9 +201,16 @@ def run_ours(args):
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if not torch.cuda.is_available():
         raise SystemExit("bench.py needs a CUDA device (no CPU fallback)")
+    # debugging aid: several ranks sharing GPU 0 (gloo collectives through the host); never a bench number
+    same_gpu = os.environ.get("SNT_BENCH_RANKS_SHARE_GPU0") == "1"
+    if same_gpu:
+        local_rank = 0
     torch.cuda.set_device(local_rank)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if same_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     lib = _native.load()
     device = torch.device("cuda", local_rank)
     hbm_peak, peak_src = measured_peaks()
@@ -443,6 +450,7 @@ def run_ours(args):
                        "parallelism": f"leaf-range sharding x{world}, shard = 2^{sp.levels} leaves",
                        "l2_policy": "inputs (6.55 GB per pass) larger than the 126 MB L2",
                        "root": root_hex},
+            **({"debug": "ranks share GPU 0 over gloo; not a measurement"} if same_gpu else {}),
             "e2e": e2e, "gpu_launches": launches, "clocks": clocks.summary(), "roofline": roofline,
             "int_pipe": int_pipe, "cpu_baseline": cpu, "dataset": dataset,
         }

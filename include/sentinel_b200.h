@@ -142,6 +142,22 @@ int snt_lthash_samples(const void* d_shard, const uint64_t* d_off, const uint64_
 int snt_lthash_model(const snt_model_plan* plan, uint64_t leaf_begin, uint64_t leaf_end,
                      uint32_t* d_acc, uint64_t* d_counts, void* d_digests, snt_stream_t stream);
 
+/* per_layer_hash, LATTICE construction (model.py:255-262): block j of tensor i is
+ * tagged LE64(i) || LE64(j) and added into slot i of d_acc[n_tensors x 32] /
+ * d_counts[n_tensors]; an empty tensor keeps the zero digest. */
+int snt_lthash_model_layers(const snt_model_plan* plan, uint64_t leaf_begin, uint64_t leaf_end,
+                            uint32_t* d_acc, uint64_t* d_counts, void* d_digests,
+                            snt_stream_t stream);
+
+/* per_layer_hash, MERKLE construction (model.py:245-253): one tree per segment.
+ * Segment t owns digests [seg_first[t], seg_first[t+1]) of d_digests (seg_first is a
+ * HOST array of n_segments + 1 entries); its root (merkle_root rule) goes to
+ * d_out + t * digest_len. An empty segment receives d_empty_digest (the digest of
+ * the empty message, model.py:247-248). */
+int snt_merkle_roots_segmented(int alg, const void* d_digests, const uint64_t* seg_first,
+                               uint32_t n_segments, const void* d_empty_digest, void* d_work,
+                               size_t work_bytes, void* d_out, snt_stream_t stream);
+
 /* lt_reduce (lattice.py:104-119): add n 64-byte digests into d_acc[32]. */
 int snt_lt_reduce(const void* d_digests, uint64_t n, uint32_t* d_acc, snt_stream_t stream);
 

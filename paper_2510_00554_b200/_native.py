@@ -43,6 +43,9 @@ SIGNATURES = {
     "snt_lthash_samples": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_uint64, c_uint32,
                                    c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "snt_lthash_model": (c_int, [c_void_p, c_uint64, c_uint64, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "snt_lthash_model_layers": (c_int, [c_void_p, c_uint64, c_uint64, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "snt_merkle_roots_segmented": (c_int, [c_int, c_void_p, POINTER(c_uint64), c_uint32, c_void_p, c_void_p,
+                                           c_size_t, c_void_p, c_void_p]),
     "snt_lt_reduce": (c_int, [c_void_p, c_uint64, c_void_p, c_void_p]),
     "snt_lt_finalize": (c_int, [c_void_p, c_uint32, c_void_p, c_void_p]),
 }

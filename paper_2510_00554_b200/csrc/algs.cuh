@@ -98,6 +98,8 @@ struct TensorTable {
 struct LeafRef {
     const uint8_t* ptr;
     uint64_t len;
+    uint32_t tensor;      // index of the owning tensor
+    uint64_t block;       // block index inside that tensor
 };
 
 SNT_HD LeafRef locate_leaf(const TensorTable& tab, uint64_t k) {
@@ -112,6 +114,8 @@ SNT_HD LeafRef locate_leaf(const TensorTable& tab, uint64_t k) {
     LeafRef r;
     r.ptr = reinterpret_cast<const uint8_t*>(tab.addr[lo]) + off;
     r.len = left < bs ? left : bs;
+    r.tensor = lo;
+    r.block = k - tab.first_leaf[lo];
     return r;
 }
 

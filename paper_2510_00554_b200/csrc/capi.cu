@@ -431,6 +431,42 @@ int snt_lthash_model(const snt_model_plan* plan, uint64_t leaf_begin, uint64_t l
                          static_cast<cudaStream_t>(stream));
 }
 
+int snt_lthash_model_layers(const snt_model_plan* plan, uint64_t leaf_begin, uint64_t leaf_end, uint32_t* d_acc,
+                            uint64_t* d_counts, void* d_digests, snt_stream_t stream) {
+    if (!plan || !d_acc || !d_counts) return SNT_ERR_INVALID_INPUT;
+    if (leaf_begin > leaf_end || leaf_end > plan->n_leaves) return SNT_ERR_INVALID_INPUT;
+    LayerLeafItems items;
+    items.tab = plan->table();
+    items.leaf_begin = leaf_begin;
+    return launch_lthash(items, leaf_end - leaf_begin, plan->n_tensors, d_acc, d_counts, d_digests, nullptr,
+                         static_cast<cudaStream_t>(stream));
+}
+
+int snt_merkle_roots_segmented(int alg, const void* d_digests, const uint64_t* seg_first, uint32_t n_segments,
+                               const void* d_empty_digest, void* d_work, size_t work_bytes, void* d_out,
+                               snt_stream_t stream) {
+    if (!valid_alg(alg)) return SNT_ERR_CONFIG;
+    if (!d_digests || !seg_first || !d_out || n_segments == 0) return SNT_ERR_INVALID_INPUT;
+    const uint32_t dlen = snt_digest_len(alg);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const uint8_t* in = static_cast<const uint8_t*>(d_digests);
+    uint8_t* out = static_cast<uint8_t*>(d_out);
+    for (uint32_t t = 0; t < n_segments; ++t) {
+        if (seg_first[t + 1] < seg_first[t]) return SNT_ERR_INVALID_INPUT;
+        const uint64_t count = seg_first[t + 1] - seg_first[t];
+        if (count == 0) {
+            if (!d_empty_digest) return SNT_ERR_INVALID_INPUT;
+            SNT_CUDA(cudaMemcpyAsync(out + static_cast<size_t>(t) * dlen, d_empty_digest, dlen,
+                                     cudaMemcpyDeviceToDevice, s));
+            continue;
+        }
+        const int rc = snt_merkle_root(alg, in + seg_first[t] * dlen, count, d_work, work_bytes,
+                                       out + static_cast<size_t>(t) * dlen, stream);
+        if (rc != SNT_OK) return rc;
+    }
+    return SNT_OK;
+}
+
 int snt_lt_reduce(const void* d_digests, uint64_t n, uint32_t* d_acc, snt_stream_t stream) {
     if (!d_acc || (n && !d_digests)) return SNT_ERR_INVALID_INPUT;
     if (n == 0) return SNT_OK;                                                        // lattice.py:112-113

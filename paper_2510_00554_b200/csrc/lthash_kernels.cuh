@@ -22,7 +22,8 @@ constexpr int LT_SMEM_SOURCES = 128;         // per-CTA shared accumulators: 128
 struct LtItem {
     const uint8_t* ptr;
     uint64_t len;
-    uint64_t tag;
+    uint64_t tag;         // first tag word: LE64(index)
+    uint64_t tag1;        // second tag word (per-layer tags LE64(layer) || LE64(block)), else unused
     uint32_t slot;
 };
 
@@ -34,11 +35,13 @@ struct SampleItems {
     const uint64_t* __restrict__ len;
     const uint64_t* __restrict__ ids;
     const uint32_t* __restrict__ slot;
+    static constexpr int TAG_WORDS = 1;
     SNT_HD LtItem get(uint64_t i) const {
         LtItem it;
         it.ptr = shard + off[i];
         it.len = len[i];
         it.tag = ids[i];
+        it.tag1 = 0;
         it.slot = slot[i];
         return it;
     }
@@ -49,6 +52,7 @@ struct SampleItems {
 struct LeafItems {
     TensorTable tab;
     uint64_t leaf_begin;
+    static constexpr int TAG_WORDS = 1;
     SNT_HD LtItem get(uint64_t i) const {
         const uint64_t k = leaf_begin + i;
         const LeafRef r = locate_leaf(tab, k);
@@ -56,7 +60,26 @@ struct LeafItems {
         it.ptr = r.ptr;
         it.len = r.len;
         it.tag = k;
+        it.tag1 = 0;
         it.slot = 0;
+        return it;
+    }
+};
+
+// Per-layer lattice hashing (model.py:255-262): block j of tensor i is tagged
+// LE64(i) || LE64(j) and summed into accumulator slot i (one slot per tensor).
+struct LayerLeafItems {
+    TensorTable tab;
+    uint64_t leaf_begin;
+    static constexpr int TAG_WORDS = 2;
+    SNT_HD LtItem get(uint64_t i) const {
+        const LeafRef r = locate_leaf(tab, leaf_begin + i);
+        LtItem it;
+        it.ptr = r.ptr;
+        it.len = r.len;
+        it.tag = r.tensor;
+        it.tag1 = r.block;
+        it.slot = r.tensor;
         return it;
     }
 };
@@ -79,7 +102,7 @@ lthash_kernel(const Items items, uint64_t n, uint32_t n_sources, uint32_t* __res
             if (status) atomicOr(status, 1u);          // undeclared source (dataset.py:78-80)
         } else {
             uint64_t h[8];
-            Blake2b::hash_message<1>(it.tag, 0, it.ptr, it.len, h);
+            Blake2b::hash_message<Items::TAG_WORDS>(it.tag, it.tag1, it.ptr, it.len, h);
             if (digests) {
                 uint4* o = reinterpret_cast<uint4*>(digests + i * 64);
 #pragma unroll
@@ -149,7 +172,8 @@ lthash_quad_kernel(const Items items, uint64_t n, uint32_t n_sources, uint32_t* 
             if (status && q.c == 0) atomicOr(status, 1u);
         } else {
             uint64_t h_lo, h_hi;
-            Blake2bQuad::hash_message<1>(regions + quad * QUAD_REGION_BYTES, q, it.tag, 0, it.ptr, it.len, h_lo, h_hi);
+            Blake2bQuad::hash_message<Items::TAG_WORDS>(regions + quad * QUAD_REGION_BYTES, q, it.tag, it.tag1, it.ptr,
+                                                        it.len, h_lo, h_hi);
             if (digests) {
                 uint64_t* o = reinterpret_cast<uint64_t*>(digests + i * 64);
                 o[q.c] = h_lo;

@@ -229,6 +229,24 @@ def merkle_reduce_levels_device(alg: str, nodes: torch.Tensor, first: int, n_in:
     return out
 
 
+def merkle_roots_segmented_device(alg: str, digests: torch.Tensor, seg_first: Sequence[int],
+                                  empty_digest: torch.Tensor) -> torch.Tensor:
+    """``snt_merkle_roots_segmented``: one tree per segment of a digest array (per-layer Merkle)."""
+    lib = _native.load()
+    dev = require_cuda()
+    dlen = DIGEST_LEN[alg]
+    n_seg = len(seg_first) - 1
+    widest = max(b - a for a, b in zip(seg_first[:-1], seg_first[1:]))
+    wb = merkle_work_bytes(alg, max(widest, 1))
+    work = torch.empty(max(wb, 16), dtype=torch.uint8, device=dev)
+    out = torch.empty(n_seg * dlen, dtype=torch.uint8, device=dev)
+    first = (ctypes.c_uint64 * (n_seg + 1))(*seg_first)
+    rc = lib.snt_merkle_roots_segmented(ALG_IDS[alg], _ptr(digests), first, n_seg, _ptr(empty_digest), _ptr(work),
+                                        wb, _ptr(out), _stream())
+    _native.check(rc, "snt_merkle_roots_segmented")
+    return out
+
+
 class LatticeAccumulator:
     """Device-resident per-source LtHash sums: ``n_sources x 32`` u32 lanes + u64 counts.
 
@@ -271,6 +289,21 @@ class LatticeAccumulator:
         lib = _native.load()
         rc = lib.snt_lt_reduce(_ptr(digests), n, _ptr(self.acc), _stream())
         _native.check(rc, "snt_lt_reduce")
+
+    def add_model_layers(self, plan: ModelPlan, leaf_begin: int, leaf_end: int) -> None:
+        """Per-layer lattice: block j of tensor i tagged LE64(i) || LE64(j), summed into slot i."""
+        lib = _native.load()
+        rc = lib.snt_lthash_model_layers(plan.handle, leaf_begin, leaf_end, _ptr(self.acc), _ptr(self.counts),
+                                         None, _stream())
+        _native.check(rc, "snt_lthash_model_layers")
+
+    def finalize_device(self) -> torch.Tensor:
+        """``n_sources x 64`` digest bytes as a device tensor (no synchronisation)."""
+        lib = _native.load()
+        out = torch.empty(self.n_sources * 64, dtype=torch.uint8, device=self.acc.device)
+        rc = lib.snt_lt_finalize(_ptr(self.acc), self.n_sources, _ptr(out), _stream())
+        _native.check(rc, "snt_lt_finalize")
+        return out
 
     def digests(self) -> Tuple[bytes, List[int], int]:
         """(n_sources x 64 digest bytes, counts, status bits); synchronises."""

@@ -104,6 +104,15 @@ class CudaBackend:
         return t.cpu().numpy().tobytes()
 
 
+def _needs_host_staging(t: torch.Tensor, group=None) -> bool:
+    """gloo cannot move CUDA tensors for every collective: stage through the host then.
+
+    NCCL (the production backend) takes the device tensors directly; this only matters for
+    debugging several ranks on one GPU and for CPU-only test runs.
+    """
+    return t.device.type == "cuda" and dist.get_backend(group) == "gloo"
+
+
 def sharded_merkle_root(backend, shard_plan: ShardPlan, rank: int, world: int, group=None) -> torch.Tensor:
     """This rank's shard roots -> all-gather -> top reduce. Returns the root (flat uint8 tensor).
 
@@ -122,8 +131,13 @@ def sharded_merkle_root(backend, shard_plan: ShardPlan, rank: int, world: int, g
         send = torch.zeros(widest * dlen, dtype=torch.uint8, device=backend.device)
         if mine:
             send[:mine * dlen].copy_(local[:mine * dlen])
-        recv = torch.empty(world * widest * dlen, dtype=torch.uint8, device=backend.device)
-        dist.all_gather_into_tensor(recv, send, group=group)
+        if _needs_host_staging(send, group):
+            host = torch.empty(world * widest * dlen, dtype=torch.uint8)
+            dist.all_gather_into_tensor(host, send.cpu(), group=group)
+            recv = host.to(backend.device)
+        else:
+            recv = torch.empty(world * widest * dlen, dtype=torch.uint8, device=backend.device)
+            dist.all_gather_into_tensor(recv, send, group=group)
         parts = [recv[r * widest * dlen:(r * widest + shard_plan.shard_count(r)) * dlen] for r in range(world)]
         nodes = torch.cat(parts)
     return backend.root_of(nodes, shard_plan.n_shards)
@@ -197,7 +211,12 @@ def allreduce_lattice(acc: torch.Tensor, counts: torch.Tensor, status: Optional[
     ``acc`` is int32 (the bit pattern of u32 lanes; two's-complement addition is
     the same sum modulo 2^32), ``counts`` int64. One all-reduce each, latency bound.
     """
-    dist.all_reduce(acc, op=dist.ReduceOp.SUM, group=group)
-    dist.all_reduce(counts, op=dist.ReduceOp.SUM, group=group)
-    if status is not None:
-        dist.all_reduce(status, op=dist.ReduceOp.MAX, group=group)
+    for t, op in ((acc, dist.ReduceOp.SUM), (counts, dist.ReduceOp.SUM), (status, dist.ReduceOp.MAX)):
+        if t is None:
+            continue
+        if _needs_host_staging(t, group):
+            host = t.cpu()
+            dist.all_reduce(host, op=op, group=group)
+            t.copy_(host)
+        else:
+            dist.all_reduce(t, op=op, group=group)

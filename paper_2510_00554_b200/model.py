@@ -25,7 +25,7 @@ import torch
 
 from . import device as _dev
 from .compression import CompressionAlg, Digest
-from .errors import ConfigError, FormatError, InvalidInput, SentinelError
+from .errors import ConfigError, FormatError, InvalidInput
 from .lattice import DIGEST_BYTES as LT_DIGEST_BYTES
 from .lattice import LatticeDigest
 
@@ -298,8 +298,77 @@ def coalesce_hash(cfg: HashConfig, model: TensorMap, workers: int = 1) -> ModelD
 
 
 def per_layer_hash(cfg: HashConfig, model: TensorMap, workers: int = 1) -> ModelDigestResult:
-    """Per-layer strategy (model.py:231-286) -- not on this round's hot path."""
-    raise SentinelError("per-layer hashing is not built yet in the B200 engine (SURVEY.md section 8(f), rank 2)")
+    """Hash each tensor to a layer digest, then reduce the layer digests (model.py:231-286).
+
+    Merkle: every tensor is its own tree over its blocks, the last block zero-padded to
+    the block size (an empty tensor contributes H(b"")), and the layer digests are the
+    leaves of a second tree in entry order. The full blocks are hashed in place; only the
+    ragged tails (< one block each) are copied into a zero-filled scratch buffer. All
+    leaves go through one leaf launch, the per-tensor trees through
+    ``snt_merkle_roots_segmented``.
+    Lattice: blocks are unpadded and tagged LE64(layer) || LE64(block); one launch sums
+    every tensor into its own accumulator slot, and the model digest is the sum of the
+    layer digests. ``ordered_per_layer`` changes the reference's schedule, not the result.
+    """
+    _require_nonempty(model)
+    dev = _dev.require_cuda()
+    bs = cfg.block_size
+    names = model.names()
+    flat = device_tensors(model)
+    sizes = [t.numel() for t in flat]
+    n_layers = len(flat)
+    block_counts = [-(-s // bs) for s in sizes]
+
+    if cfg.construction is Construction.MERKLE:
+        alg = cfg.alg.value
+        dlen = cfg.alg.digest_len
+        ragged = [i for i, s in enumerate(sizes) if s % bs]
+        scratch = torch.zeros(max(1, len(ragged)) * bs, dtype=torch.uint8, device=dev)
+        virt: List[torch.Tensor] = []
+        seg_first = [0]
+        slot = 0
+        for i, t in enumerate(flat):
+            full = (sizes[i] // bs) * bs
+            if full:
+                virt.append(t[:full])
+            if sizes[i] % bs:
+                pad = scratch[slot * bs:(slot + 1) * bs]
+                pad[:sizes[i] - full].copy_(t[full:])
+                virt.append(pad)
+                slot += 1
+            seg_first.append(seg_first[-1] + block_counts[i])
+        plan = _dev.ModelPlan(virt, bs)
+        try:
+            hasher = _dev.MerkleModelHasher(plan, alg)
+            hasher.run_leaves_only()
+            empty = _dev.hash_blocks_device(alg, None, torch.zeros(1, dtype=torch.int64, device=dev),
+                                            torch.zeros(1, dtype=torch.int64, device=dev))
+            layers_dev = _dev.merkle_roots_segmented_device(alg, hasher.leaves, seg_first, empty)
+            root_dev = _dev.merkle_root_device(alg, layers_dev, n_layers)
+            layer_bytes = layers_dev.cpu().numpy().tobytes()
+            root = Digest(cfg.alg, root_dev.cpu().numpy().tobytes())
+            aux_digest = hasher.leaves.numel() + layers_dev.numel() + hasher.work_bytes
+            aux_data = scratch.numel() if ragged else 0
+        finally:
+            plan.close()
+        layer_digests = {name: Digest(cfg.alg, layer_bytes[i * dlen:(i + 1) * dlen]) for i, name in enumerate(names)}
+        return ModelDigestResult(root, cfg, sum(block_counts), layer_digests=layer_digests,
+                                 aux_data_bytes=aux_data, aux_digest_bytes=aux_digest)
+
+    plan = _dev.ModelPlan(flat, bs)
+    try:
+        acc = _dev.LatticeAccumulator(n_layers)
+        acc.add_model_layers(plan, 0, plan.leaf_count)
+        layers_dev = acc.finalize_device()
+        total = _dev.LatticeAccumulator(1)
+        total.add_digests(layers_dev, n_layers)
+        layer_bytes = layers_dev.cpu().numpy().tobytes()
+        model_bytes, _, _ = total.digests()
+    finally:
+        plan.close()
+    layer_digests = {name: LatticeDigest(layer_bytes[i * 64:(i + 1) * 64]) for i, name in enumerate(names)}
+    return ModelDigestResult(LatticeDigest(model_bytes), cfg, sum(block_counts), layer_digests=layer_digests,
+                             aux_digest_bytes=(n_layers + 1) * _dev.LT_LANES * 4)
 
 
 def ordered_lattice_per_layer(cfg: HashConfig, model: TensorMap, workers: int = 1) -> ModelDigestResult:

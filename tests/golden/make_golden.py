@@ -100,6 +100,17 @@ def model_cases():
                 rec["n_blocks"] = r.block_count
                 rec[f"merkle_coalesced_{alg}"] = hash_model(
                     HashConfig(Construction.MERKLE, Strategy.COALESCED, ALGS[alg], bs), tm).digest_hex()
+                pl = hash_model(HashConfig(Construction.MERKLE, Strategy.PER_LAYER, ALGS[alg], bs), tm)
+                rec[f"merkle_per_layer_{alg}"] = pl.digest_hex()
+                rec[f"merkle_layers_sha256_{alg}"] = hashlib.sha256(
+                    b"".join(d.data for d in pl.layer_digests.values())).hexdigest()
+                rec["per_layer_block_count"] = pl.block_count
+            pl = hash_model(HashConfig(Construction.LATTICE, Strategy.PER_LAYER, CompressionAlg.BLAKE2B, bs), tm)
+            rec["lattice_per_layer"] = pl.digest_hex()
+            rec["lattice_layers_sha256"] = hashlib.sha256(b"".join(d.data for d in pl.layer_digests.values())).hexdigest()
+            po = hash_model(HashConfig(Construction.LATTICE, Strategy.PER_LAYER, CompressionAlg.BLAKE2B, bs,
+                                       ordered_per_layer=True), tm)
+            assert po.digest_hex() == pl.digest_hex()
             rec["lattice_inplace"] = hash_model(
                 HashConfig(Construction.LATTICE, Strategy.IN_PLACE, CompressionAlg.BLAKE2B, bs), tm).digest_hex()
             rec["lattice_coalesced"] = hash_model(

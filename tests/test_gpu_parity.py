@@ -168,6 +168,20 @@ def test_seeded_models_root_and_every_leaf(pkg, golden):
             assert hasher.out_bytes().hex() == rec[f"merkle_inplace_{name}"]
             cfg_c = pkg.HashConfig(pkg.Construction.MERKLE, pkg.Strategy.COALESCED, _alg(pkg, name), bs)
             assert pkg.hash_model(cfg_c, model).digest_hex() == rec[f"merkle_coalesced_{name}"]
+            cfg_p = pkg.HashConfig(pkg.Construction.MERKLE, pkg.Strategy.PER_LAYER, _alg(pkg, name), bs)
+            pl = pkg.hash_model(cfg_p, model)
+            assert pl.digest_hex() == rec[f"merkle_per_layer_{name}"], (rec["case"], bs, name)
+            assert list(pl.layer_digests) == model.names()
+            assert hashlib.sha256(b"".join(d.data for d in pl.layer_digests.values())).hexdigest() == \
+                rec[f"merkle_layers_sha256_{name}"]
+            assert pl.block_count == rec["per_layer_block_count"]
+        for ordered in (False, True):
+            cfg_l = pkg.HashConfig(pkg.Construction.LATTICE, pkg.Strategy.PER_LAYER, pkg.CompressionAlg.BLAKE2B, bs,
+                                   ordered_per_layer=ordered)
+            pl = pkg.hash_model(cfg_l, model)
+            assert pl.digest_hex() == rec["lattice_per_layer"], (rec["case"], bs, ordered)
+            assert hashlib.sha256(b"".join(d.data for d in pl.layer_digests.values())).hexdigest() == \
+                rec["lattice_layers_sha256"]
         lat = pkg.HashConfig(pkg.Construction.LATTICE, pkg.Strategy.IN_PLACE, pkg.CompressionAlg.BLAKE2B, bs)
         assert pkg.hash_model(lat, model).digest_hex() == rec["lattice_inplace"], (rec["case"], bs)
         lat_c = pkg.HashConfig(pkg.Construction.LATTICE, pkg.Strategy.COALESCED, pkg.CompressionAlg.BLAKE2B, bs)
@@ -212,6 +226,24 @@ def test_host_model_staged_in_overlapped_chunks(pkg, corc, monkeypatch):
         res = pkg.hash_model(cfg, pkg.TensorMap(entries))
         assert res.model_digest.data == corc.inplace_merkle(name, tl, 8192, 4), name
         assert res.block_count == tl.leaf_count(8192)
+
+
+def test_per_layer_full_size_vgg19_against_oracle(pkg, porc):
+    """38 layer digests of the VGG19 layout (scaled) for both constructions, against the oracle."""
+    sd = _synthetic("vgg19", scale=0.06)
+    model = pkg.TensorMap(list(sd))
+    host = [t.cpu().numpy().tobytes() for _, t in sd]
+    for name in ("sha256", "sha3-256"):
+        res = pkg.hash_model(pkg.HashConfig(pkg.Construction.MERKLE, pkg.Strategy.PER_LAYER, _alg(pkg, name)), model)
+        root, layers = porc.per_layer_merkle(name, host, 8192)
+        assert len(res.layer_digests) == 38
+        assert [d.data for d in res.layer_digests.values()] == layers and res.model_digest.data == root
+    res = pkg.hash_model(pkg.HashConfig(pkg.Construction.LATTICE, pkg.Strategy.PER_LAYER, pkg.CompressionAlg.BLAKE2B), model)
+    root, layers = porc.per_layer_lattice(host, 8192)
+    assert [d.data for d in res.layer_digests.values()] == layers and res.model_digest.data == root
+    with pytest.raises(pkg.errors.ConfigError):
+        pkg.ordered_lattice_per_layer(pkg.HashConfig(pkg.Construction.LATTICE, pkg.Strategy.PER_LAYER,
+                                                     pkg.CompressionAlg.BLAKE2B), model)
 
 
 def test_empty_model_and_bad_config(pkg):

@@ -86,6 +86,12 @@ def test_seeded_models(golden, porc, corc):
             assert c_leaves == bytes(leaves)
             assert corc.inplace_merkle(alg, tl, bs, threads=2) == want
             assert porc.coalesced_merkle(alg, tensors, bs).hex() == rec[f"merkle_coalesced_{alg}"]
+            root, layers = porc.per_layer_merkle(alg, tensors, bs)
+            assert root.hex() == rec[f"merkle_per_layer_{alg}"]
+            assert hashlib.sha256(b"".join(layers)).hexdigest() == rec[f"merkle_layers_sha256_{alg}"]
+        root, layers = porc.per_layer_lattice(tensors, bs)
+        assert root.hex() == rec["lattice_per_layer"]
+        assert hashlib.sha256(b"".join(layers)).hexdigest() == rec["lattice_layers_sha256"]
         assert porc.inplace_lattice(tensors, bs, workers=3).hex() == rec["lattice_inplace"]
         assert corc.inplace_lattice(tl, bs, threads=3).hex() == rec["lattice_inplace"]
         assert porc.coalesced_lattice(tensors, bs).hex() == rec["lattice_coalesced"]
