@@ -14,7 +14,10 @@ from typing import Optional
 
 from .errors import ResourceError, raise_for_status
 
-LIB_PATH = Path(__file__).resolve().parent / "lib" / "libsentinel_b200.so"
+import os
+
+# SNT_LIB_PATH lets kernel experiments (tools/) load an alternative build of the same ABI
+LIB_PATH = Path(os.environ.get("SNT_LIB_PATH") or Path(__file__).resolve().parent / "lib" / "libsentinel_b200.so")
 
 SNT_LEVELS_TO_ROOT = 0xFFFFFFFF
 ABI_VERSION = 1

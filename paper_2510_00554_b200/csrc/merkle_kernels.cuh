@@ -13,6 +13,13 @@
 namespace snt {
 
 constexpr int LEAF_THREADS = 128;
+// Minimum resident CTAs per SM the SHA-256 leaf kernel is compiled for. Occupancy itself does
+// not matter (the kernel runs at the same speed with 2 to 8 CTAs per SM); the register cap
+// selects among ptxas allocations whose bank-conflict behaviour differs by ~3%
+// (profiles/r1_leafbench_occ.jsonl: 71 regs 7.23 ms, 64 regs 7.47 ms, 56 regs 7.27 ms).
+#ifndef SNT_LEAF_MINB
+#define SNT_LEAF_MINB 1
+#endif
 constexpr int REDUCE_THREADS = 256;
 
 // ---- leaf hashing -----------------------------------------------------------
@@ -73,8 +80,14 @@ SNT_D void load_digest(const uint8_t* in, uint32_t* d) {
 // path. The irregular leaves (ragged tensor tails, tensors at odd addresses)
 // are listed in `irregular` and hashed by the first `irr_ctas` CTAs of the same
 // grid with the generic path, concurrently with the rest.
+// The generic path is kept out of line so that it does not take part in the register
+// allocation and instruction scheduling of the regular-leaf loop.
+__device__ __noinline__ void sha256_leaf_generic(const uint8_t* p, uint64_t len, uint32_t one, uint32_t d[8]) {
+    Sha256::hash_message(p, len, d, one);
+}
+
 template <int ALG>
-__global__ void __launch_bounds__(LEAF_THREADS)
+__global__ void __launch_bounds__(LEAF_THREADS, (ALG == ALG_SHA256) ? SNT_LEAF_MINB : 1)
 merkle_leaf_kernel(const TensorTable tab, const __grid_constant__ MerkleConsts c,
                    uint64_t leaf_begin, uint64_t leaf_end, const uint64_t* __restrict__ irregular,
                    uint32_t n_irregular, uint32_t irr_ctas, uint8_t* __restrict__ d_leaves) {
@@ -87,7 +100,7 @@ merkle_leaf_kernel(const TensorTable tab, const __grid_constant__ MerkleConsts c
             const uint64_t k = irregular[j];
             if (k < leaf_begin || k >= leaf_end) return;
             const LeafRef leaf = locate_leaf(tab, k);
-            A::leaf(leaf.ptr, leaf.len, c, d);
+            sha256_leaf_generic(leaf.ptr, leaf.len, c.one, d);
             store_digest<ALG>(d_leaves + (k - leaf_begin) * A::DIGEST_BYTES, d);
             return;
         }

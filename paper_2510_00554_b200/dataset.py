@@ -102,9 +102,14 @@ class DeviceDataset:
         """Copy host arrays to the device. ``source_of_sample`` holds source ids, not slots."""
         dev = _dev.require_cuda()
         source_ids = sorted(set(int(s) for s in source_ids))
-        lut = {sid: i for i, sid in enumerate(source_ids)}
-        src = np.asarray(source_of_sample)
-        slots = np.fromiter((lut.get(int(s), -1) for s in src), dtype=np.int64, count=src.size)
+        src = np.asarray(source_of_sample, dtype=np.int64)
+        table = np.asarray(source_ids, dtype=np.int64)
+        slots = np.searchsorted(table, src)
+        if table.size:
+            hit = table[np.minimum(slots, table.size - 1)] == src
+        else:
+            hit = np.zeros(src.shape, dtype=bool)
+        slots = np.where(hit, slots, -1)
         bad = np.nonzero(slots < 0)[0]
         if bad.size:
             i = int(bad[0])

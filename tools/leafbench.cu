@@ -121,13 +121,16 @@ static uint64_t g_leaves;
 static Params g_prm;
 static std::vector<uint8_t> h_ref, h_out;
 
+static size_t g_dyn_smem = 0;
+
 template <int THREADS, int MINB, int IMAD, int WIDE, int HINT>
 static void run(const char* name, bool is_ref = false) {
     const unsigned grid = static_cast<unsigned>((g_leaves + THREADS - 1) / THREADS);
     cudaFuncAttributes attr;
     CHECK(cudaFuncGetAttributes(&attr, leaf_kernel<THREADS, MINB, IMAD, WIDE, HINT>));
+    CHECK(cudaFuncSetAttribute(leaf_kernel<THREADS, MINB, IMAD, WIDE, HINT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CHECK(cudaMemset(g_out, 0, g_leaves * 32));
-    leaf_kernel<THREADS, MINB, IMAD, WIDE, HINT><<<grid, THREADS>>>(g_data, g_leaves, g_prm, is_ref ? g_ref : g_out);
+    leaf_kernel<THREADS, MINB, IMAD, WIDE, HINT><<<grid, THREADS, g_dyn_smem>>>(g_data, g_leaves, g_prm, is_ref ? g_ref : g_out);
     CHECK(cudaDeviceSynchronize());
     int ok = 1;
     if (is_ref) {
@@ -143,7 +146,7 @@ static void run(const char* name, bool is_ref = false) {
     const int reps = 5;
     for (int r = 0; r < reps; ++r) {
         CHECK(cudaEventRecord(e0));
-        leaf_kernel<THREADS, MINB, IMAD, WIDE, HINT><<<grid, THREADS>>>(g_data, g_leaves, g_prm, g_out);
+        leaf_kernel<THREADS, MINB, IMAD, WIDE, HINT><<<grid, THREADS, g_dyn_smem>>>(g_data, g_leaves, g_prm, g_out);
         CHECK(cudaEventRecord(e1));
         CHECK(cudaEventSynchronize(e1));
         float ms;
@@ -153,9 +156,9 @@ static void run(const char* name, bool is_ref = false) {
     }
     CHECK(cudaGetLastError());
     const double bytes = double(g_leaves) * 8192;
-    printf("{\"variant\": \"%s\", \"threads\": %d, \"minb\": %d, \"imad\": %d, \"wide\": %d, \"hint\": %d, \"regs\": %d, "
+    printf("{\"dyn_smem_kb\": %d, \"variant\": \"%s\", \"threads\": %d, \"minb\": %d, \"imad\": %d, \"wide\": %d, \"hint\": %d, \"regs\": %d, "
            "\"ok\": %d, \"best_ms\": %.4f, \"avg_ms\": %.4f, \"gbs_best\": %.1f}\n",
-           name, THREADS, MINB, IMAD, WIDE, HINT, attr.numRegs, ok, best, sum / reps, bytes / (best * 1e-3) / 1e9);
+           (int)(g_dyn_smem / 1024), name, THREADS, MINB, IMAD, WIDE, HINT, attr.numRegs, ok, best, sum / reps, bytes / (best * 1e-3) / 1e9);
     fflush(stdout);
 }
 
@@ -195,5 +198,14 @@ int main(int argc, char** argv) {
     run<128, 1, 1, 0, 1>("t128+imad ld.nc default");
     run<128, 1, 1, 0, 2>("t128+imad ldg256 evict_first");
     run<128, 1, 1, 1, 2>("t128 wide+imad ldg256 evict_first");
+    run<128, 8, 1, 0, 0>("t128 minb8 (<=64 regs)+imad");
+    run<128, 9, 1, 0, 0>("t128 minb9 (<=56 regs)+imad");
+    // occupancy sweep for the default kernel: CTAs/SM limited by dynamic shared memory
+    for (int ctas : {7, 6, 5, 4, 3, 2}) {
+        g_dyn_smem = (size_t)(224 * 1024 / ctas) & ~1023u;
+        run<128, 1, 1, 0, 0>("t128+imad occupancy sweep");
+        run<128, 8, 1, 0, 0>("t128 minb8+imad occupancy sweep");
+    }
+    g_dyn_smem = 0;
     return 0;
 }
