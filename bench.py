@@ -399,23 +399,8 @@ def run_ours(args):
             ds_e2e()
         barrier()
         ds_dt = (time.perf_counter() - t0) / 5
-        # the two kernel variants side by side (same digests; auto picks by item count)
-        variants = {}
-        for mode, label in ((1, "thread_per_sample_ms"), (2, "quad_per_sample_ms")):
-            lib.snt_debug_lthash_mode(mode)
-            for _ in range(2):
-                ds_step()
-            torch.cuda.synchronize()
-            v0, v1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            v0.record()
-            for _ in range(args.steps):
-                ds_step()
-            v1.record()
-            torch.cuda.synchronize()
-            variants[label] = round(v0.elapsed_time(v1) / args.steps, 4)
-        lib.snt_debug_lthash_mode(0)
         dataset = {"metric": "cifar10_shaped_lthash_samples_per_s", "value": round(n / (ds_ms * 1e-3), 1),
-                   "kernel_variants": variants,
+
                    "unit": "samples/s", "ms_per_step": round(ds_ms, 4), "samples": n, "bytes": n * ln,
                    "gbs": round(n * ln / (ds_ms * 1e-3) / 1e9, 2),
                    "e2e": {"value": round(n / ds_dt, 1), "unit": "samples/s", "ms_per_step": round(ds_dt * 1e3, 3),

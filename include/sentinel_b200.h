@@ -46,9 +46,6 @@ const char* snt_last_cuda_error(void);
 uint32_t snt_abi_version(void);
 /* Diagnostic: kernels launched by this library in this process so far. */
 uint64_t snt_debug_launch_count(void);
-/* Diagnostic/test knob for the LtHash kernels: 0 = choose by item count (default),
- * 1 = one thread per item, 2 = four lanes per item. Results are identical. */
-void snt_debug_lthash_mode(int mode);
 /* 32, 64, 32 -- or 0 for an unknown algorithm. */
 uint32_t snt_digest_len(int alg);
 

@@ -28,7 +28,6 @@ SIGNATURES = {
     "snt_last_cuda_error": (c_char_p, []),
     "snt_abi_version": (c_uint32, []),
     "snt_debug_launch_count": (c_uint64, []),
-    "snt_debug_lthash_mode": (None, [c_int]),
     "snt_digest_len": (c_uint32, [c_int]),
     "snt_model_plan_create": (c_int, [POINTER(c_void_p), POINTER(c_uint64), c_uint32, c_uint32, c_void_p,
                                       POINTER(c_void_p)]),

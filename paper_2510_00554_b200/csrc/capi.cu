@@ -247,7 +247,7 @@ int launch_leaves(const snt_model_plan* plan, uint64_t begin, uint64_t end, uint
     const uint64_t grid = (n + LEAF_THREADS - 1) / LEAF_THREADS + irr_ctas;
     if (grid > 0x7fffffffull) return SNT_ERR_INVALID_INPUT;
     const uint64_t* irregular = plan->d_table + 3ull * plan->n_tensors + 1;
-    merkle_leaf_kernel<ALG><<<static_cast<unsigned>(grid), LEAF_THREADS, 0, s>>>(
+    merkle_leaf_kernel<ALG><<<static_cast<unsigned>(grid), LEAF_THREADS, leaf_stage_bytes<ALG>(), s>>>(
         plan->table(), plan->consts, begin, end, irregular, plan->n_irregular, irr_ctas, d_leaves);
     SNT_CUDA(cudaGetLastError());
     ++g_launches;
@@ -259,18 +259,12 @@ int launch_blocks(const uint8_t* base, const uint64_t* off, const uint64_t* len,
                   uint8_t* out, cudaStream_t s) {
     const uint64_t grid = (n + LEAF_THREADS - 1) / LEAF_THREADS;
     if (grid > 0x7fffffffull) return SNT_ERR_INVALID_INPUT;
-    hash_blocks_kernel<ALG><<<static_cast<unsigned>(grid), LEAF_THREADS, 0, s>>>(base, off, len, n, node_consts(), out);
+    hash_blocks_kernel<ALG><<<static_cast<unsigned>(grid), LEAF_THREADS, leaf_stage_bytes<ALG>(), s>>>(
+        base, off, len, n, node_consts(), out);
     SNT_CUDA(cudaGetLastError());
     ++g_launches;
     return SNT_OK;
 }
-
-// Item counts below this would use four lanes per item (lthash_quad_kernel). Measured on B200
-// (CIFAR-shaped 50k x 3 KiB: 0.277 ms quad vs 0.216 ms one thread per item; profiles/) the quad
-// form loses: its G functions have no instruction-level parallelism left and every round adds
-// 12 shuffles. It stays selectable through snt_debug_lthash_mode for experiments and tests.
-constexpr uint64_t LT_QUAD_MAX_ITEMS = 0;
-std::atomic<int> g_lthash_mode{0};       // debug knob: 0 auto, 1 one thread per item, 2 quad
 
 template <class Items>
 int launch_lthash(const Items& items, uint64_t n, uint32_t n_sources, uint32_t* d_acc,
@@ -278,29 +272,15 @@ int launch_lthash(const Items& items, uint64_t n, uint32_t n_sources, uint32_t* 
     if (n == 0) return SNT_OK;
     auto* counts = reinterpret_cast<unsigned long long*>(d_counts);
     auto* dig = static_cast<uint8_t*>(d_digests);
-    const bool smem_acc = n_sources <= static_cast<uint32_t>(LT_SMEM_SOURCES);
-    const size_t acc_bytes = smem_acc ? static_cast<size_t>(n_sources) * (LT_LANES + 1) * sizeof(uint32_t) : 0;
-    const int mode = g_lthash_mode.load();
-    const bool quad = mode == 2 || (mode == 0 && n < LT_QUAD_MAX_ITEMS);   // LT_QUAD_MAX_ITEMS == 0: never by default
-    if (quad) {
-        const uint64_t grid = (n + LTQ_QUADS - 1) / LTQ_QUADS;
-        if (grid > 0x7fffffffull) return SNT_ERR_INVALID_INPUT;
-        const size_t smem = static_cast<size_t>(LTQ_QUADS) * QUAD_REGION_BYTES + acc_bytes;
-        if (smem_acc)
-            lthash_quad_kernel<Items, true><<<static_cast<unsigned>(grid), LTQ_THREADS, smem, s>>>(
-                items, n, n_sources, d_acc, counts, dig, d_status);
-        else
-            lthash_quad_kernel<Items, false><<<static_cast<unsigned>(grid), LTQ_THREADS, smem, s>>>(
-                items, n, n_sources, d_acc, counts, dig, d_status);
+    const uint64_t grid = (n + LT_THREADS - 1) / LT_THREADS;
+    if (grid > 0x7fffffffull) return SNT_ERR_INVALID_INPUT;
+    if (n_sources <= static_cast<uint32_t>(LT_SMEM_SOURCES)) {
+        const size_t smem = LT_STAGE_BYTES + static_cast<size_t>(n_sources) * (LT_LANES + 1) * sizeof(uint32_t);
+        lthash_kernel<Items, true><<<static_cast<unsigned>(grid), LT_THREADS, smem, s>>>(
+            items, n, n_sources, d_acc, counts, dig, d_status);
     } else {
-        const uint64_t grid = (n + LT_THREADS - 1) / LT_THREADS;
-        if (grid > 0x7fffffffull) return SNT_ERR_INVALID_INPUT;
-        if (smem_acc)
-            lthash_kernel<Items, true><<<static_cast<unsigned>(grid), LT_THREADS, acc_bytes, s>>>(
-                items, n, n_sources, d_acc, counts, dig, d_status);
-        else
-            lthash_kernel<Items, false><<<static_cast<unsigned>(grid), LT_THREADS, 0, s>>>(
-                items, n, n_sources, d_acc, counts, dig, d_status);
+        lthash_kernel<Items, false><<<static_cast<unsigned>(grid), LT_THREADS, LT_STAGE_BYTES, s>>>(
+            items, n, n_sources, d_acc, counts, dig, d_status);
     }
     SNT_CUDA(cudaGetLastError());
     ++g_launches;
@@ -310,8 +290,6 @@ int launch_lthash(const Items& items, uint64_t n, uint32_t n_sources, uint32_t* 
 }  // namespace
 
 extern "C" {
-
-void snt_debug_lthash_mode(int mode) { g_lthash_mode.store(mode); }
 
 int snt_merkle_leaves(const snt_model_plan* plan, int alg, uint64_t leaf_begin, uint64_t leaf_end,
                       void* d_leaves, snt_stream_t stream) {

@@ -11,7 +11,7 @@
 //   model.py:183-193    _lattice_sum_blocks with tag LE64(k) (model.py:312)
 #pragma once
 #include "algs.cuh"
-#include "blake2b_quad.cuh"
+#include "blake2b_staged.cuh"
 
 namespace snt {
 
@@ -84,12 +84,18 @@ struct LayerLeafItems {
     }
 };
 
+// Dynamic shared memory: the per-thread message staging buffers (blake2b_staged.cuh), then
+// (SMEM_ACC) the per-CTA accumulators [n_sources][32] lanes + [n_sources] counts.
+constexpr size_t LT_STAGE_BYTES = 2ull * B2S_SLOTS * LT_THREADS * sizeof(uint64_t);
+
 template <class Items, bool SMEM_ACC>
 __global__ void __launch_bounds__(LT_THREADS)
 lthash_kernel(const Items items, uint64_t n, uint32_t n_sources, uint32_t* __restrict__ acc,
               unsigned long long* __restrict__ counts, uint8_t* __restrict__ digests,
               uint32_t* __restrict__ status) {
-    extern __shared__ uint32_t sacc[];       // [n_sources][32] lanes, then [n_sources] counts
+    extern __shared__ __align__(16) uint8_t lt_smem[];
+    uint64_t* stage = reinterpret_cast<uint64_t*>(lt_smem) + threadIdx.x;
+    uint32_t* sacc = reinterpret_cast<uint32_t*>(lt_smem + LT_STAGE_BYTES);
     uint32_t* scnt = sacc + static_cast<size_t>(n_sources) * LT_LANES;
     if (SMEM_ACC) {
         for (uint32_t i = threadIdx.x; i < n_sources * (LT_LANES + 1); i += LT_THREADS) sacc[i] = 0;
@@ -102,7 +108,7 @@ lthash_kernel(const Items items, uint64_t n, uint32_t n_sources, uint32_t* __res
             if (status) atomicOr(status, 1u);          // undeclared source (dataset.py:78-80)
         } else {
             uint64_t h[8];
-            Blake2b::hash_message<Items::TAG_WORDS>(it.tag, it.tag1, it.ptr, it.len, h);
+            Blake2bStaged<LT_THREADS>::template hash_message<Items::TAG_WORDS>(stage, it.tag, it.tag1, it.ptr, it.len, h);
             if (digests) {
                 uint4* o = reinterpret_cast<uint4*>(digests + i * 64);
 #pragma unroll
@@ -139,65 +145,6 @@ lthash_kernel(const Items items, uint64_t n, uint32_t n_sources, uint32_t* __res
             if (v) atomicAdd(acc + j, v);
         }
         for (uint32_t j = threadIdx.x; j < n_sources; j += LT_THREADS) {
-            const uint32_t v = scnt[j];
-            if (v) atomicAdd(counts + j, static_cast<unsigned long long>(v));
-        }
-    }
-}
-
-// Four lanes per item (blake2b_quad.cuh): the variant for item counts that cannot fill the
-// GPU with one thread per item. Same accumulator protocol as lthash_kernel.
-constexpr int LTQ_THREADS = 128;
-constexpr int LTQ_QUADS = LTQ_THREADS / 4;
-
-template <class Items, bool SMEM_ACC>
-__global__ void __launch_bounds__(LTQ_THREADS)
-lthash_quad_kernel(const Items items, uint64_t n, uint32_t n_sources, uint32_t* __restrict__ acc,
-                   unsigned long long* __restrict__ counts, uint8_t* __restrict__ digests,
-                   uint32_t* __restrict__ status) {
-    extern __shared__ __align__(16) uint8_t smem_raw[];
-    uint8_t* regions = smem_raw;                                             // LTQ_QUADS x 144 B
-    uint32_t* sacc = reinterpret_cast<uint32_t*>(smem_raw + LTQ_QUADS * QUAD_REGION_BYTES);
-    uint32_t* scnt = sacc + static_cast<size_t>(n_sources) * LT_LANES;
-    if (SMEM_ACC) {
-        for (uint32_t i = threadIdx.x; i < n_sources * (LT_LANES + 1); i += LTQ_THREADS) sacc[i] = 0;
-        __syncthreads();
-    }
-    const QuadLane q = quad_lane();
-    const uint32_t quad = threadIdx.x >> 2;
-    const uint64_t i = static_cast<uint64_t>(blockIdx.x) * LTQ_QUADS + quad;
-    if (i < n) {
-        const LtItem it = items.get(i);
-        if (it.slot >= n_sources) {
-            if (status && q.c == 0) atomicOr(status, 1u);
-        } else {
-            uint64_t h_lo, h_hi;
-            Blake2bQuad::hash_message<Items::TAG_WORDS>(regions + quad * QUAD_REGION_BYTES, q, it.tag, it.tag1, it.ptr,
-                                                        it.len, h_lo, h_hi);
-            if (digests) {
-                uint64_t* o = reinterpret_cast<uint64_t*>(digests + i * 64);
-                o[q.c] = h_lo;
-                o[4 + q.c] = h_hi;
-            }
-            uint32_t* dst = (SMEM_ACC ? sacc : acc) + static_cast<size_t>(it.slot) * LT_LANES;
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                atomicAdd(dst + 4 * q.c + k, static_cast<uint32_t>(h_lo >> (16 * k)) & 0xffffu);
-                atomicAdd(dst + 16 + 4 * q.c + k, static_cast<uint32_t>(h_hi >> (16 * k)) & 0xffffu);
-            }
-            if (q.c == 0) {
-                if (SMEM_ACC) atomicAdd(scnt + it.slot, 1u);
-                else atomicAdd(counts + it.slot, 1ull);
-            }
-        }
-    }
-    if (SMEM_ACC) {
-        __syncthreads();
-        for (uint32_t j = threadIdx.x; j < n_sources * LT_LANES; j += LTQ_THREADS) {
-            const uint32_t v = sacc[j];
-            if (v) atomicAdd(acc + j, v);
-        }
-        for (uint32_t j = threadIdx.x; j < n_sources; j += LTQ_THREADS) {
             const uint32_t v = scnt[j];
             if (v) atomicAdd(counts + j, static_cast<unsigned long long>(v));
         }

@@ -9,6 +9,7 @@
 //   root         merkle.py:152-165 (single leaf is returned unchanged)
 #pragma once
 #include "algs.cuh"
+#include "blake2b_staged.cuh"
 
 namespace snt {
 
@@ -80,6 +81,29 @@ SNT_D void load_digest(const uint8_t* in, uint32_t* d) {
 // path. The irregular leaves (ragged tensor tails, tensors at odd addresses)
 // are listed in `irregular` and hashed by the first `irr_ctas` CTAs of the same
 // grid with the generic path, concurrently with the rest.
+// Dynamic shared memory a leaf-hashing CTA needs: BLAKE2b prefetches its message through two
+// staging buffers per thread (blake2b_staged.cuh); the other algorithms load straight to registers.
+template <int ALG>
+constexpr size_t leaf_stage_bytes() {
+    return ALG == ALG_BLAKE2B ? 2ull * B2S_SLOTS * LEAF_THREADS * sizeof(uint64_t) : 0;
+}
+
+// One leaf / block with the algorithm's preferred formulation.
+template <int ALG>
+SNT_D void hash_one_leaf(const uint8_t* p, uint64_t len, const MerkleConsts& c, uint32_t* d) {
+    using A = AlgTraits<ALG>;
+    if (ALG == ALG_BLAKE2B) {
+        extern __shared__ __align__(16) uint8_t leaf_smem[];
+        uint64_t* stage = reinterpret_cast<uint64_t*>(leaf_smem) + threadIdx.x;
+        uint64_t h[8];
+        Blake2bStaged<LEAF_THREADS>::template hash_message<0>(stage, 0, 0, p, len, h);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) { d[2 * i] = static_cast<uint32_t>(h[i]); d[2 * i + 1] = static_cast<uint32_t>(h[i] >> 32); }
+    } else {
+        A::leaf(p, len, c, d);
+    }
+}
+
 // The generic path is kept out of line so that it does not take part in the register
 // allocation and instruction scheduling of the regular-leaf loop.
 __device__ __noinline__ void sha256_leaf_generic(const uint8_t* p, uint64_t len, uint32_t one, uint32_t d[8]) {
@@ -116,7 +140,7 @@ merkle_leaf_kernel(const TensorTable tab, const __grid_constant__ MerkleConsts c
         const uint64_t k = leaf_begin + static_cast<uint64_t>(blockIdx.x) * LEAF_THREADS + threadIdx.x;
         if (k >= leaf_end) return;
         const LeafRef leaf = locate_leaf(tab, k);
-        A::leaf(leaf.ptr, leaf.len, c, d);
+        hash_one_leaf<ALG>(leaf.ptr, leaf.len, c, d);
         store_digest<ALG>(d_leaves + (k - leaf_begin) * A::DIGEST_BYTES, d);
     }
 }
@@ -132,7 +156,7 @@ hash_blocks_kernel(const uint8_t* __restrict__ base, const uint64_t* __restrict_
     const uint64_t i = static_cast<uint64_t>(blockIdx.x) * LEAF_THREADS + threadIdx.x;
     if (i >= n) return;
     uint32_t d[A::DW];
-    A::leaf(base + off[i], len[i], c, d);
+    hash_one_leaf<ALG>(base + off[i], len[i], c, d);
     store_digest<ALG>(out + i * A::DIGEST_BYTES, d);
 }
 

@@ -6,6 +6,7 @@
 #include <cstring>
 #include <vector>
 
+#include "../../paper_2510_00554_b200/csrc/blake2b_staged.cuh"
 #include "../../paper_2510_00554_b200/csrc/lthash_kernels.cuh"
 #include "../../paper_2510_00554_b200/csrc/merkle_kernels.cuh"
 
@@ -83,6 +84,19 @@ int hc_blake2b_tagged(int T, uint64_t tag0, uint64_t tag1, const uint8_t* p, uin
     if (T == 0) Blake2b::hash_message<0>(tag0, tag1, p, len, h);
     else if (T == 1) Blake2b::hash_message<1>(tag0, tag1, p, len, h);
     else if (T == 2) Blake2b::hash_message<2>(tag0, tag1, p, len, h);
+    else return -1;
+    memcpy(out, h, 64);
+    return 0;
+}
+
+// the shared-memory staged BLAKE2b (blake2b_staged.cuh) with the stager as a memcpy
+int hc_blake2b_staged(int T, uint64_t tag0, uint64_t tag1, const uint8_t* p, uint64_t len, uint8_t* out) {
+    uint64_t h[8];
+    uint64_t bufs[2 * B2S_SLOTS];
+    memset(bufs, 0xA5, sizeof(bufs));        // stale slots must never leak into a block
+    if (T == 0) Blake2bStaged<1>::hash_message<0>(bufs, tag0, tag1, p, len, h);
+    else if (T == 1) Blake2bStaged<1>::hash_message<1>(bufs, tag0, tag1, p, len, h);
+    else if (T == 2) Blake2bStaged<1>::hash_message<2>(bufs, tag0, tag1, p, len, h);
     else return -1;
     memcpy(out, h, 64);
     return 0;

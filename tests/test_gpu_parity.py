@@ -436,16 +436,13 @@ def test_many_sources_take_the_global_accumulator_path(pkg, corc):
     assert out == want_sums and counts == want_counts
 
 
-@pytest.mark.parametrize("mode", [1, 2])
-def test_lthash_kernel_variants_agree_with_oracle(pkg, corc, mode):
-    """One thread per item (mode 1) and four lanes per item (mode 2): ragged, unaligned, empty samples."""
-    from paper_2510_00554_b200 import _native
+def test_lthash_ragged_unaligned_and_empty_samples(pkg, corc):
+    """Every byte alignment, lengths around the BLAKE2b block boundaries, empty samples; also the model path."""
     from paper_2510_00554_b200 import dataset as ds
     from paper_2510_00554_b200 import device as dev
 
-    lib = _native.load()
     n, n_src = 2500, 7
-    rng = np.random.default_rng(40 + mode)
+    rng = np.random.default_rng(41)
     lens = rng.choice([0, 1, 7, 8, 9, 119, 120, 121, 127, 128, 129, 247, 248, 249, 256, 1000, 3072], size=n).astype(np.uint64)
     lens[:200] = rng.integers(0, 5000, size=200)
     gaps = rng.integers(0, 5, size=n).astype(np.uint64)            # every byte alignment
@@ -457,23 +454,90 @@ def test_lthash_kernel_variants_agree_with_oracle(pkg, corc, mode):
     ids = rng.integers(0, 2**63, size=n).astype(np.uint64)
     want_sums, want_counts, want_digests = corc.lthash_samples(shard, offs, lens, ids, src.astype(np.uint32), n_src, 4,
                                                                want_digests=True)
-    lib.snt_debug_lthash_mode(mode)
-    try:
-        dset = ds.DeviceDataset.from_host(shard, offs, lens, ids, src, list(range(n_src)))
-        acc = dev.LatticeAccumulator(n_src)
-        per_sample = torch.empty(n * 64, dtype=torch.uint8, device="cuda")
-        dset.accumulate(acc, digests=per_sample)
-        out, counts, status = acc.digests()
-        # the model lattice path (leaf items) through the same kernel variant
-        tensors = inputs.model_tensors(17, [40000, 123, 8192 * 3, 9999, 1, 2, 70001])
-        cfg = pkg.HashConfig(pkg.Construction.LATTICE, pkg.Strategy.IN_PLACE, pkg.CompressionAlg.BLAKE2B, 1024)
-        got_model = pkg.hash_model(cfg, pkg.TensorMap([(f"t{i}", t) for i, t in enumerate(tensors)])).model_digest.data
-    finally:
-        lib.snt_debug_lthash_mode(0)
+    dset = ds.DeviceDataset.from_host(shard, offs, lens, ids, src, list(range(n_src)))
+    acc = dev.LatticeAccumulator(n_src)
+    per_sample = torch.empty(n * 64, dtype=torch.uint8, device="cuda")
+    dset.accumulate(acc, digests=per_sample)
+    out, counts, status = acc.digests()
+    # the model lattice path (leaf items) through the same kernel
+    tensors = inputs.model_tensors(17, [40000, 123, 8192 * 3, 9999, 1, 2, 70001])
+    cfg = pkg.HashConfig(pkg.Construction.LATTICE, pkg.Strategy.IN_PLACE, pkg.CompressionAlg.BLAKE2B, 1024)
+    got_model = pkg.hash_model(cfg, pkg.TensorMap([(f"t{i}", t) for i, t in enumerate(tensors)])).model_digest.data
     assert status == 0
     assert per_sample.cpu().numpy().tobytes() == want_digests
     assert out == want_sums and counts == want_counts
     assert got_model == corc.inplace_lattice(corc.TensorList(tensors), 1024, 2)
+
+
+def test_sharded_entry_point_on_one_rank_and_sparse_staging(pkg, porc):
+    """hash_model_sharded with world == 1 equals hash_model; a rank stages only the tensors it needs."""
+    from paper_2510_00554_b200 import distributed as dd
+
+    tensors = inputs.model_tensors(16, [40000, 123, 8192 * 3, 9999, 1, 2, 70001, 8192 * 300 + 5])
+    model = pkg.TensorMap([(f"t{i}", t) for i, t in enumerate(tensors)])
+    for name in ALGS:
+        cfg = pkg.HashConfig(pkg.Construction.MERKLE, pkg.Strategy.IN_PLACE, _alg(pkg, name), 8192)
+        want = porc.inplace_merkle(name, tensors, 8192)
+        assert dd.hash_model_sharded(cfg, model, 0, 1).model_digest.data == want
+    # emulate rank r of a 3-rank job without a process group: its shard roots from sparsely staged tensors
+    from paper_2510_00554_b200 import device as dev
+    sizes = [len(t) for t in tensors]
+    first = dd._first_leaves(sizes, 8192)
+    sp = dd.plan_shards(first[-1], 3, levels=4)
+    parts = []
+    for rank in range(3):
+        a, b = sp.leaf_range(rank)
+        if b <= a:
+            continue
+        placeholder = torch.zeros(16, dtype=torch.uint8, device="cuda")
+        staged = [dev.as_device_bytes(t) if (first[i] < b and first[i + 1] > a) else placeholder
+                  for i, t in enumerate(tensors)]
+        plan = dev.ModelPlan(staged, 8192, sizes_override=sizes)
+        h = dev.MerkleModelHasher(plan, "sha256", a, b, sp.levels)
+        h.run()
+        parts.append(h.out.clone())
+    nodes = torch.cat(parts)
+    assert dev.merkle_root_device("sha256", nodes, sp.n_shards).cpu().numpy().tobytes() == \
+        porc.inplace_merkle("sha256", tensors, 8192)
+
+
+def test_multi_curator_dataset_sign_and_verify(pkg):
+    """BASELINE config 5 shape: per-source LtHash on the GPU, one P-256 key per curator on the host."""
+    samples = inputs.dataset_samples(**inputs.DATASET_CASES[2])          # 16 sources
+    acc = pkg.SourceAccumulator()
+    acc.declare(inputs.DATASET_CASES[2]["declared"])
+    pkg.process_batch(pkg.Batch([pkg.SampleRecord(*s) for s in samples]), acc)
+    digests = pkg.finalize(acc)
+    keys = {sid: pkg.keygen() for sid in digests}
+    bundles = {}
+    for sid, (digest, count) in digests.items():
+        stmt = pkg.Statement([pkg.Subject(f"ds:source:{sid}", {"lthash": digest.hex()})],
+                             pkg.attestation.DATASET_PREDICATE_TYPE,
+                             {"source_id": sid, "sample_count": count, "cover_labels": False,
+                              "index_encoding": "le64-prefix-v1"})
+        bundles[sid] = pkg.sign_bundle(stmt, keys[sid])
+    # verifier: recompute on the GPU in another order / batching, check every curator's bundle
+    acc2 = pkg.SourceAccumulator()
+    acc2.declare(inputs.DATASET_CASES[2]["declared"])
+    recs = [pkg.SampleRecord(*s) for s in reversed(samples)]
+    for start in range(0, len(recs), 33):
+        pkg.process_batch(pkg.Batch(recs[start:start + 33]), acc2)
+    fresh = pkg.finalize(acc2)
+    for sid, bundle in bundles.items():
+        name = f"ds:source:{sid}"
+        assert pkg.verify_bundle(bundle, {name: {"lthash": fresh[sid][0].hex()}}) is pkg.Verdict.OK
+        other = next(k for k in keys if k != sid)
+        forged = pkg.Bundle({"public_key": keys[other].public_point_hex}, bundle.envelope)
+        assert pkg.verify_bundle(forged, {name: {"lthash": fresh[sid][0].hex()}}) is pkg.Verdict.SIGNATURE_INVALID
+    # drop one sample of one source: only that curator's bundle fails
+    victim = samples[0][1]
+    acc3 = pkg.SourceAccumulator()
+    acc3.declare(inputs.DATASET_CASES[2]["declared"])
+    pkg.process_batch(pkg.Batch([pkg.SampleRecord(*s) for s in samples[1:]]), acc3)
+    tampered = pkg.finalize(acc3)
+    for sid, bundle in bundles.items():
+        verdict = pkg.verify_bundle(bundle, {f"ds:source:{sid}": {"lthash": tampered[sid][0].hex()}})
+        assert verdict is (pkg.Verdict.DIGEST_MISMATCH if sid == victim else pkg.Verdict.OK)
 
 
 def test_sign_and_verify_gpu_digests_end_to_end(pkg):

@@ -100,6 +100,24 @@ def test_tagged_blake2b_layouts(hc, golden):
         assert bytes(out).hex() == rec["digest"]
 
 
+def test_staged_blake2b_block_tail_and_carry_logic(hc):
+    """blake2b_staged.cuh: chunk staging, sliding tag window, tails, every alignment (host stager)."""
+    rng = random.Random(6)
+    lengths = [0, 1, 7, 8, 9, 104, 111, 112, 113, 119, 120, 121, 127, 128, 129, 240, 247, 248, 249, 255, 256, 257,
+               383, 384, 3072, 8192]
+    for t in (0, 1, 2):
+        for n in lengths + [rng.randint(0, 5000) for _ in range(60)]:
+            for shift in (0, 8, rng.randint(1, 7), rng.randint(9, 15)):
+                data = rng.randbytes(n)
+                keep, p = _aligned(data, shift)
+                t0, t1 = rng.getrandbits(64), rng.getrandbits(64)
+                out = (ctypes.c_uint8 * 64)()
+                assert hc.hc_blake2b_staged(t, ctypes.c_uint64(t0), ctypes.c_uint64(t1), ctypes.c_void_p(p),
+                                            ctypes.c_uint64(n), out) == 0
+                tag = [b"", struct.pack("<Q", t0), struct.pack("<QQ", t0, t1)][t]
+                assert bytes(out) == hashlib.blake2b(tag + data).digest(), (t, n, shift)
+
+
 def test_leaf_locator_equals_block_table(hc):
     """locate_leaf (per-tensor table + binary search) == the reference's per-block rows (model.py:137-146)."""
     from paper_2510_00554_b200.model import BlockTable, TensorMap
