@@ -312,13 +312,22 @@ def run_ours(args):
         cfg = pkg.HashConfig(pkg.Construction.MERKLE, pkg.Strategy.IN_PLACE, pkg.CompressionAlg.from_name(args.alg))
         host_entries = []
         seen = {}
+        first_leaf = 0
+        my_a, my_b = sp.leaf_range(rank)
         for name, t in sd:
-            key = t.data_ptr()
+            nbytes = t.numel() * 4
+            next_leaf = first_leaf + -(-nbytes // 8192)
+            mine = world == 1 or (first_leaf < my_b and next_leaf > my_a)
+            key = (t.data_ptr(), mine)
             if key not in seen:
-                h = torch.empty(t.numel() * 4, dtype=torch.uint8).pin_memory()
-                h.copy_(t.reshape(-1).view(torch.uint8))
+                if mine:
+                    h = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+                    h.copy_(t.reshape(-1).view(torch.uint8))
+                else:
+                    h = torch.empty(nbytes, dtype=torch.uint8)   # never read by this rank: not pinned, not touched
                 seen[key] = h
             host_entries.append((name, seen[key]))
+            first_leaf = next_leaf
         torch.cuda.synchronize()
         if world == 1:
             model = pkg.TensorMap(host_entries)

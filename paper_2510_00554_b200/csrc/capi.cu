@@ -188,16 +188,32 @@ size_t snt_merkle_work_bytes(int alg, uint64_t count) {
 
 namespace {
 
+// CTA size of the level reducer, by grid size. Every CTA walks its levels one barrier at a
+// time, so a launch is as slow as (critical path of one CTA) x (number of waves):
+//   <= 5/SM   -> 256 threads (512 threads were measured no faster: with 16 warps per CTA the
+//                first level is ALU-bound instead of latency-bound, same time);
+//   more      -> 128 threads: twice as many CTAs fit per SM (registers), fewer waves
+//                (BLAKE2b / SHA3-256 trees of 800k leaves: -8% / -4%; SHA-256 neutral).
+template <int ALG, int THREADS>
+int launch_reduce_t(const uint8_t* in, uint64_t first, uint64_t n_in, uint64_t level_count, uint32_t levels,
+                    const MerkleConsts& c, uint8_t* out, uint64_t n_out, cudaStream_t s) {
+    static const cudaError_t carve = cudaFuncSetAttribute(
+        merkle_reduce_kernel<ALG, THREADS>, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+    (void)carve;
+    merkle_reduce_kernel<ALG, THREADS><<<static_cast<unsigned>(n_out), THREADS, 0, s>>>(
+        in, first, n_in, level_count, levels, c, out);
+    SNT_CUDA(cudaGetLastError());
+    ++g_launches;
+    return SNT_OK;
+}
+
 template <int ALG>
 int launch_reduce(const uint8_t* in, uint64_t first, uint64_t n_in, uint64_t level_count,
                   uint32_t levels, const MerkleConsts& c, uint8_t* out, cudaStream_t s) {
     const uint64_t n_out = cdiv_shift(n_in, levels);
     if (n_out > 0x7fffffffull) return SNT_ERR_INVALID_INPUT;
-    merkle_reduce_kernel<ALG><<<static_cast<unsigned>(n_out), REDUCE_THREADS, 0, s>>>(
-        in, first, n_in, level_count, levels, c, out);
-    SNT_CUDA(cudaGetLastError());
-    ++g_launches;
-    return SNT_OK;
+    if (n_out <= 5 * 148) return launch_reduce_t<ALG, 256>(in, first, n_in, level_count, levels, c, out, n_out, s);
+    return launch_reduce_t<ALG, 128>(in, first, n_in, level_count, levels, c, out, n_out, s);
 }
 
 int launch_reduce_alg(int alg, const uint8_t* in, uint64_t first, uint64_t n_in, uint64_t level_count,

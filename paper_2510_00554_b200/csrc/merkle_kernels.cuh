@@ -21,7 +21,7 @@ constexpr int LEAF_THREADS = 128;
 #ifndef SNT_LEAF_MINB
 #define SNT_LEAF_MINB 1
 #endif
-constexpr int REDUCE_THREADS = 256;
+constexpr int REDUCE_THREADS = 256;       // default CTA size of the level reducer (see launch_reduce)
 
 // ---- leaf hashing -----------------------------------------------------------
 
@@ -198,8 +198,8 @@ SNT_D void pair_or_pad(uint32_t* left, const uint32_t* right, bool right_exists,
     for (int i = 0; i < A::DW; ++i) left[i] = out[i];
 }
 
-template <int ALG>
-__global__ void __launch_bounds__(REDUCE_THREADS)
+template <int ALG, int THREADS>
+__global__ void __launch_bounds__(THREADS)
 merkle_reduce_kernel(const uint8_t* __restrict__ in, uint64_t first, uint64_t n_in,
                      uint64_t level_count, uint32_t levels, const __grid_constant__ MerkleConsts c,
                      uint8_t* __restrict__ out) {
@@ -215,7 +215,7 @@ merkle_reduce_kernel(const uint8_t* __restrict__ in, uint64_t first, uint64_t n_
     const uint32_t width = 1u << levels;
 
     // level 0 -> 1 straight from global memory: pair p = inputs base + 2p, base + 2p + 1
-    for (uint32_t p = tid; p < (width >> 1); p += REDUCE_THREADS) {
+    for (uint32_t p = tid; p < (width >> 1); p += THREADS) {
         const uint64_t g = base + 2ull * p;
         if (g < in_end) {
             uint32_t l[DW], r[DW];
@@ -236,7 +236,7 @@ merkle_reduce_kernel(const uint8_t* __restrict__ in, uint64_t first, uint64_t n_
         const uint32_t n_out = width >> (t + 1);
         const uint64_t cnt = ceil_shift(level_count, t);          // nodes the tree has at this level
         const uint64_t gbase = base >> t;
-        for (uint32_t p = tid; p < n_out; p += REDUCE_THREADS) {
+        for (uint32_t p = tid; p < n_out; p += THREADS) {
             const uint64_t g = gbase + 2ull * p;
             if (g < cnt) {
                 uint32_t l[DW], r[DW];
