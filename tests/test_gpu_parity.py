@@ -265,9 +265,11 @@ def _synthetic(arch, scale=1.0):
     return shapes.synthetic_state_dict(arch, torch.device("cuda"), seed=0, scale=scale)
 
 
-@pytest.mark.parametrize("arch,alg", [("gpt2", "sha256"), ("vgg19", "blake2b"), ("vgg19", "sha3-256")])
+@pytest.mark.parametrize("arch,alg", [("gpt2", "sha256"), ("gpt2-xl", "sha256"),
+                                      ("vgg19", "blake2b"), ("vgg19", "sha3-256"),
+                                      ("bert-large", "blake2b"), ("bert-large", "sha3-256")])
 def test_full_size_models_against_c_oracle(pkg, corc, arch, alg):
-    """BASELINE configs 1 and 4 at full size: root AND every leaf digest, bit-exact."""
+    """BASELINE configs 1, 2 and 4 at full size: root AND every leaf digest, bit-exact."""
     from paper_2510_00554_b200 import device as dev
 
     sd = _synthetic(arch)
@@ -399,7 +401,7 @@ def test_hellaswag_shaped_variable_length_samples(pkg, corc):
     from paper_2510_00554_b200 import dataset as ds
     from paper_2510_00554_b200 import device as dev
 
-    n, n_src = 4000, 16
+    n, n_src = 40_000, 16
     rng = np.random.default_rng(2)
     toks = np.clip(np.round(rng.lognormal(np.log(90), 0.4, size=n)), 16, 256).astype(np.int64)
     lens = (toks * 4).astype(np.uint64)
@@ -414,6 +416,26 @@ def test_hellaswag_shaped_variable_length_samples(pkg, corc):
     out, counts, _ = acc.digests()
     want_sums, want_counts = corc.lthash_samples(shard, offs, lens, ids, src.astype(np.uint32), n_src, 4)
     assert out == want_sums and counts == want_counts
+    assert sum(counts) == n
+
+
+def test_other_block_sizes_at_scale(pkg, corc):
+    """Block sizes 64 B and 1 MiB over a 48 MB ragged model (tree depth 20 and 6)."""
+    from paper_2510_00554_b200 import device as dev
+
+    rng = np.random.default_rng(21)
+    sizes = [(20 << 20) + 77, 3, (1 << 20), (26 << 20) + 4096 + 5, 64, 8191]
+    host = [rng.integers(0, 256, size=s, dtype=np.uint8) for s in sizes]
+    flat = [torch.from_numpy(h).cuda() for h in host]
+    tl = corc.TensorList(host)
+    for bs, algs in ((64, ["sha256"]), (1 << 20, ALGS)):
+        plan = dev.ModelPlan(flat, bs)
+        for name in algs:
+            h = dev.MerkleModelHasher(plan, name)
+            h.run()
+            want_leaves = corc.inplace_leaves(name, tl, bs, corc.threads_default())
+            assert h.leaf_bytes() == want_leaves, (bs, name)
+            assert h.out_bytes() == corc.merkle_root(name, want_leaves, plan.leaf_count, 4), (bs, name)
 
 
 def test_many_sources_take_the_global_accumulator_path(pkg, corc):
