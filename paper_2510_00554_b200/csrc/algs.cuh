@@ -19,6 +19,21 @@ struct MerkleConsts {
     uint32_t one;                   // 1, opaque to the compiler (Sha256::add_fma)
 };
 
+// A per-thread register holding 1 that ptxas cannot fold (loaded through a lane-indexed constant
+// read), for the IMAD form that carries a round constant in its immediate slot (Sha256::addk_fma).
+#ifdef __CUDACC__
+__constant__ uint32_t k_lane_ones[32] = {1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1,
+                                         1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1};
+#endif
+SNT_HD Sha256::One sha256_one(const MerkleConsts& c) {
+#ifdef __CUDA_ARCH__
+    return Sha256::One(c.one, k_lane_ones[threadIdx.x & 31]);
+#else
+    (void)c;
+    return Sha256::One();
+#endif
+}
+
 template <int ALG> struct AlgTraits;
 
 template <> struct AlgTraits<ALG_SHA256> {
@@ -28,10 +43,10 @@ template <> struct AlgTraits<ALG_SHA256> {
     SNT_HD static uint32_t to_mem(uint32_t w) { return bswap32(w); }
     SNT_HD static uint32_t from_mem(uint32_t w) { return bswap32(w); }
     SNT_HD static void leaf(const uint8_t* p, uint64_t len, const MerkleConsts& c, uint32_t d[DW]) {
-        Sha256::hash_message(p, len, d, c.one);
+        Sha256::hash_message(p, len, d, sha256_one(c));
     }
     SNT_HD static void pair(const uint32_t* l, const uint32_t* r, const MerkleConsts& c, uint32_t* out) {
-        Sha256::hash_pair(l, r, c.sha256_pad_node, out, c.one);
+        Sha256::hash_pair(l, r, c.sha256_pad_node, out, sha256_one(c));
     }
 };
 

@@ -29,7 +29,7 @@ constexpr int REDUCE_THREADS = 256;       // default CTA size of the level reduc
 // 16-byte aligned: 4 x LDG.128 per compression with the next block's loads
 // issued before the current block's rounds, then the constant padding block.
 SNT_HD void sha256_leaf_aligned(const uint8_t* __restrict__ p, uint32_t nblk,
-                               const uint32_t* __restrict__ pad_kw, uint32_t s[8], uint32_t one = 1u) {
+                               const uint32_t* __restrict__ pad_kw, uint32_t s[8], const Sha256::One& one = Sha256::One()) {
     Sha256::init(s);
     U4 q0 = ld128(p), q1 = ld128(p + 16), q2 = ld128(p + 32), q3 = ld128(p + 48);
 #pragma unroll 1
@@ -45,7 +45,7 @@ SNT_HD void sha256_leaf_aligned(const uint8_t* __restrict__ p, uint32_t nblk,
         }
         Sha256::compress(s, w, one);
     }
-    Sha256::compress_const(s, pad_kw);
+    Sha256::compress_const(s, pad_kw, one);
 }
 
 template <int ALG>
@@ -106,8 +106,9 @@ SNT_D void hash_one_leaf(const uint8_t* p, uint64_t len, const MerkleConsts& c, 
 
 // The generic path is kept out of line so that it does not take part in the register
 // allocation and instruction scheduling of the regular-leaf loop.
-__device__ __noinline__ void sha256_leaf_generic(const uint8_t* p, uint64_t len, uint32_t one, uint32_t d[8]) {
-    Sha256::hash_message(p, len, d, one);
+__device__ __noinline__ void sha256_leaf_generic(const uint8_t* p, uint64_t len, uint32_t one_u, uint32_t one_v,
+                                                 uint32_t d[8]) {
+    Sha256::hash_message(p, len, d, Sha256::One(one_u, one_v));
 }
 
 template <int ALG>
@@ -118,13 +119,14 @@ merkle_leaf_kernel(const TensorTable tab, const __grid_constant__ MerkleConsts c
     using A = AlgTraits<ALG>;
     uint32_t d[A::DW];
     if (ALG == ALG_SHA256) {
+        const Sha256::One one = sha256_one(c);
         if (blockIdx.x < irr_ctas) {
             const uint32_t j = blockIdx.x * LEAF_THREADS + threadIdx.x;
             if (j >= n_irregular) return;
             const uint64_t k = irregular[j];
             if (k < leaf_begin || k >= leaf_end) return;
             const LeafRef leaf = locate_leaf(tab, k);
-            sha256_leaf_generic(leaf.ptr, leaf.len, c.one, d);
+            sha256_leaf_generic(leaf.ptr, leaf.len, one.u, one.v, d);
             store_digest<ALG>(d_leaves + (k - leaf_begin) * A::DIGEST_BYTES, d);
             return;
         }
@@ -134,7 +136,7 @@ merkle_leaf_kernel(const TensorTable tab, const __grid_constant__ MerkleConsts c
         const bool regular = leaf.len == (1ull << tab.block_shift) &&
                              (reinterpret_cast<uintptr_t>(leaf.ptr) & 15) == 0;
         if (!regular) return;                              // hashed by the irregular CTAs
-        sha256_leaf_aligned(leaf.ptr, 1u << (tab.block_shift - 6), c.sha256_pad_leaf, d, c.one);
+        sha256_leaf_aligned(leaf.ptr, 1u << (tab.block_shift - 6), c.sha256_pad_leaf, d, one);
         store_digest<ALG>(d_leaves + (k - leaf_begin) * A::DIGEST_BYTES, d);
     } else {
         const uint64_t k = leaf_begin + static_cast<uint64_t>(blockIdx.x) * LEAF_THREADS + threadIdx.x;

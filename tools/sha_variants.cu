@@ -14,6 +14,7 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <string>
 
 #include "../paper_2510_00554_b200/csrc/sha256.cuh"
 
@@ -29,6 +30,7 @@
 struct Consts {
     uint32_t one;
     uint32_t p[32];    // p[n] = 2^(32-n) for n in 1..31
+    const uint32_t* ones;   // device array of 1s: a load the compiler cannot see through (per-thread register)
 };
 
 __device__ __forceinline__ uint64_t mulwide(uint32_t x, uint32_t m) {
@@ -50,8 +52,21 @@ __device__ __forceinline__ uint32_t madd(uint32_t a, uint32_t one, uint32_t b) {
 template <int SS, int SB, int AD>
 struct V {
     const Consts& c;
-    __device__ V(const Consts& cc) : c(cc) {}
+    uint32_t vone;
+    __device__ V(const Consts& cc) : c(cc), vone(cc.ones[threadIdx.x & 31]) {}
+    static __device__ __forceinline__ uint32_t maddk(uint32_t one_v, uint32_t k, uint32_t x) {
+        uint32_t r;
+        asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(one_v), "r"(k), "r"(x));   // k folds to an immediate
+        return r;
+    }
+    // x >> n as the high half of x * 2^(32-n): IMAD.HI on the FMA pipe (half rate), one vector operand
+    __device__ __forceinline__ uint32_t shr_hi(uint32_t x, int n) const {
+        uint32_t r;
+        asm("mul.hi.u32 %0, %1, %2;" : "=r"(r) : "r"(x), "r"(c.p[n]));
+        return r;
+    }
     __device__ __forceinline__ uint32_t ssig0(uint32_t x) const {
+        if (AD == 6 || AD == 7 || AD == 10) return snt::rotr32(x, 7) ^ snt::rotr32(x, 18) ^ shr_hi(x, 3);
         if (SS) {
             const uint64_t a = mulwide(x, c.p[7]), b = mulwide(x, c.p[18]), d = mulwide(x, c.p[3]);
             return lo32(a) ^ hi32(a) ^ lo32(b) ^ hi32(b) ^ hi32(d);
@@ -59,6 +74,7 @@ struct V {
         return snt::Sha256::ssig0(x);
     }
     __device__ __forceinline__ uint32_t ssig1(uint32_t x) const {
+        if (AD == 6 || AD == 7 || AD == 10 || AD == 11) return snt::rotr32(x, 17) ^ snt::rotr32(x, 19) ^ shr_hi(x, 10);
         if (SS) {
             const uint64_t a = mulwide(x, c.p[17]), b = mulwide(x, c.p[19]), d = mulwide(x, c.p[10]);
             return lo32(a) ^ hi32(a) ^ lo32(b) ^ hi32(b) ^ hi32(d);
@@ -80,7 +96,7 @@ struct V {
         return snt::Sha256::bsig1(x);
     }
     __device__ __forceinline__ uint32_t add_sched(uint32_t a, uint32_t b) const {
-        return (AD == 1 || AD == 2) ? madd(a, c.one, b) : a + b;
+        return (AD == 1 || AD == 2 || AD >= 4) ? madd(a, c.one, b) : a + b;
     }
     __device__ __forceinline__ uint32_t add_fma(uint32_t a, uint32_t b) const {
         return (AD == 1 || AD == 3) ? madd(a, c.one, b) : a + b;
@@ -97,6 +113,26 @@ struct V {
                 const uint32_t x = add_sched(w[t & 15], w[(t - 7) & 15]);
                 const uint32_t y = add_sched(ssig1(w[(t - 2) & 15]), ssig0(w[(t - 15) & 15]));
                 w[t & 15] = add_sched(x, y);
+            }
+            if (AD >= 8) {
+                // 8: only (h + K + w) stays an ALU IADD3 (K in its immediate slot); 9: K enters through
+                // IMAD(vone, K, h) with a per-thread register holding 1, so no addition is left on the ALU pipe
+                const uint32_t hkw = (AD == 8) ? h + K[t] + w[t & 15]
+                                               : madd(maddk(vone, K[t], h), c.one, w[t & 15]);
+                const uint32_t t1 = madd(hkw, c.one, madd(bsig1(e), c.one, snt::Sha256::ch(e, f, g)));
+                const uint32_t na = madd(t1, c.one, madd(bsig0(a), c.one, snt::Sha256::maj(a, b, cc)));
+                h = g; g = f; f = e; e = madd(d, c.one, t1); d = cc; cc = b; b = a; a = na;
+                continue;
+            }
+            if (AD >= 4) {
+                // K rides in the immediate slot of an ALU IADD3; the two-input additions go to IMAD with
+                // the multiplier in a uniform register (two vector operands per instruction)
+                const uint32_t t1 = (h + K[t] + w[t & 15]) + (bsig1(e) + snt::Sha256::ch(e, f, g));
+                uint32_t na;
+                if (AD == 5 || AD == 6) na = madd(t1, c.one, madd(bsig0(a), c.one, snt::Sha256::maj(a, b, cc)));
+                else na = t1 + bsig0(a) + snt::Sha256::maj(a, b, cc);
+                h = g; g = f; f = e; e = (AD == 7) ? d + t1 : madd(d, c.one, t1); d = cc; cc = b; b = a; a = na;
+                continue;
             }
             const uint32_t hk = add_fma(add_fma(h, K[t]), w[t & 15]);          // off the critical path
             const uint32_t t1 = add_any(add_any(hk, snt::Sha256::ch(e, f, g)), bsig1(e));
@@ -162,7 +198,7 @@ static void run(const char* name, int sms, int ctas_per_sm) {
            name, SS, SB, AD, ctas_per_sm * 4, ok, comp * 64 / (best * 1e-3) / 1e9);
 }
 
-int main() {
+int main(int argc, char** argv) {
     cudaDeviceProp prop;
     CHECK(cudaGetDeviceProperties(&prop, 0));
     const int sms = prop.multiProcessorCount;
@@ -171,13 +207,47 @@ int main() {
     g_c.one = 1;
     for (int n = 1; n < 32; ++n) g_c.p[n] = 1u << (32 - n);
     g_c.p[0] = 0;
+    {
+        uint32_t h_ones[32];
+        for (int i = 0; i < 32; ++i) h_ones[i] = 1;
+        uint32_t* d_ones;
+        CHECK(cudaMalloc(&d_ones, sizeof(h_ones)));
+        CHECK(cudaMemcpy(d_ones, h_ones, sizeof(h_ones), cudaMemcpyHostToDevice));
+        g_c.ones = d_ones;
+    }
     variant_kernel<0, 0, 0><<<4, 128>>>(g_ref, 3, 99u, g_c, 1);
     CHECK(cudaDeviceSynchronize());
+    if (argc > 1) {      // one variant only (for ncu): sha_variants <name> [ctas_per_sm]
+        const std::string v = argv[1];
+        const int occ = argc > 2 ? atoi(argv[2]) : 8;
+        if (v == "stock") run<0, 0, 0>("stock", sms, occ);
+        else if (v == "adds_imad") run<0, 0, 1>("adds_imad", sms, occ);
+        else if (v == "sched_adds_imad") run<0, 0, 2>("sched_adds_imad", sms, occ);
+        else if (v == "hkw_adds_imad") run<0, 0, 3>("hkw_adds_imad", sms, occ);
+        else if (v == "sched_e") run<0, 0, 4>("sched_e", sms, occ);
+        else if (v == "sched_e_a") run<0, 0, 5>("sched_e_a", sms, occ);
+        else if (v == "sched_e_a_shr") run<0, 0, 6>("sched_e_a_shr", sms, occ);
+        else if (v == "sched_shr") run<0, 0, 7>("sched_shr", sms, occ);
+        else if (v == "all_but_hkw") run<0, 0, 8>("all_but_hkw", sms, occ);
+        else if (v == "all_adds_ur") run<0, 0, 9>("all_adds_ur", sms, occ);
+        else if (v == "all_adds_ur_shr") run<0, 0, 10>("all_adds_ur_shr", sms, occ);
+        else if (v == "all_adds_ur_shr1") run<0, 0, 11>("all_adds_ur_shr1", sms, occ);
+        else { fprintf(stderr, "unknown variant\n"); return 2; }
+        return 0;
+    }
     for (int occ : {8, 16}) {
         run<0, 0, 0>("stock", sms, occ);
         run<0, 0, 1>("adds_imad", sms, occ);
         run<0, 0, 2>("sched_adds_imad", sms, occ);
         run<0, 0, 3>("hkw_adds_imad", sms, occ);
+        run<0, 0, 4>("sched_e", sms, occ);
+        run<0, 0, 5>("sched_e_a", sms, occ);
+        run<0, 0, 6>("sched_e_a_shr", sms, occ);
+        run<0, 0, 7>("sched_shr", sms, occ);
+        run<0, 0, 8>("all_but_hkw", sms, occ);
+        run<0, 0, 9>("all_adds_ur", sms, occ);
+        run<0, 0, 10>("all_adds_ur_shr", sms, occ);
+        run<0, 0, 11>("all_adds_ur_shr1", sms, occ);
         run<1, 0, 0>("ssig_wide", sms, occ);
         run<1, 0, 3>("ssig_wide+hkw_imad", sms, occ);
         run<1, 0, 2>("ssig_wide+sched_imad", sms, occ);
