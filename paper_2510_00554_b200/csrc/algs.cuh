@@ -46,7 +46,10 @@ template <> struct AlgTraits<ALG_SHA256> {
         Sha256::hash_message(p, len, d, sha256_one(c));
     }
     SNT_HD static void pair(const uint32_t* l, const uint32_t* r, const MerkleConsts& c, uint32_t* out) {
-        Sha256::hash_pair(l, r, c.sha256_pad_node, out, sha256_one(c));
+        // Compile-time ones: the additions fold back to 3-input IADD3. The level reducer is bound by the
+        // latency of one node hash per level, and the IMAD formulation has the longer dependency chain
+        // (tree of 799,954 digests: 200.8 us vs 206.0 us; 79,672: 68.6 vs 76.8; tools/tree_probe.py).
+        Sha256::hash_pair(l, r, c.sha256_pad_node, out);
     }
 };
 

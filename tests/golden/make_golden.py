@@ -177,7 +177,27 @@ def attestation_cases():
     }
 
 
+def bench_cases():
+    """Digest column of the reference's strategy-comparison table (bench.py:81-133) on small synthetic
+    models, plus a fingerprint of the synthetic bytes themselves (bench.py:32-45)."""
+    from sentinel import bench as rbench
+
+    out = {"models": [], "cells": []}
+    for shape, scale, seed in (("vgg19", 0.0005, 0), ("resnet152", 0.002, 0), ("gpt2", 0.0003, 5)):
+        m = rbench.synthetic_model(shape, scale, seed)
+        out["models"].append({"shape": shape, "scale": scale, "seed": seed, "layers": len(m.entries),
+                              "total_bytes": m.total_bytes,
+                              "sha256_of_bytes": hashlib.sha256(b"".join(b for _, b in m.entries)).hexdigest()})
+    for c in rbench.run_bench(shapes=("vgg19", "resnet152"), scale=0.002, worker_counts=(1,), repeats=1,
+                              compressions=("sha256", "blake2b", "sha3-256")):
+        out["cells"].append({"shape": c.shape, "construction": c.construction, "compression": c.compression,
+                             "strategy": c.strategy, "digest": c.digest})
+    return out
+
+
 def main():
+    (HERE / "golden_bench.json").write_text(json.dumps(bench_cases(), indent=1, sort_keys=True))
+    print("wrote", HERE / "golden_bench.json")
     doc = {
         "generator": "tests/golden/make_golden.py",
         "reference": f"sentinel {sentinel.__version__} imported from /root/reference/pkg/src",

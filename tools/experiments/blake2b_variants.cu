@@ -1,0 +1,166 @@
+// BLAKE2b formulation experiments (compute-only, message from registers).
+//
+// The stock compilation puts all 22 32-bit instructions of a G on the ALU pipe (8 for the four 64-bit
+// additions, 8 LOP3, 4 PRMT, 2 SHF). A 64-bit addition can instead run on the FMA pipe as
+//   IMAD.WIDE.U32 t, a.lo, ONE, b      (t = b + a.lo with the carry into the high word; half rate)
+//   IMAD          t.hi, a.hi, ONE, t.hi
+// with ONE = 1 in a uniform register, i.e. at most two vector operands (or one + a register pair) per
+// instruction -- the form that still dual-issues with the ALU pipe (tools/pipe_mix.cu).
+// Variants: CF = how many of the two `c = c + d` additions of a G go to the FMA pipe, AF = how many of
+// the two `a = a + b + m` additions (each is two 64-bit two-input additions there).
+// Every variant is checked against the stock compression on the same input.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <string>
+
+#include "../../paper_2510_00554_b200/csrc/blake2b.cuh"
+
+#define CHECK(x)                                                                      \
+    do {                                                                              \
+        cudaError_t e = (x);                                                          \
+        if (e != cudaSuccess) {                                                       \
+            fprintf(stderr, "%s: %s\n", #x, cudaGetErrorString(e));                   \
+            exit(1);                                                                  \
+        }                                                                             \
+    } while (0)
+
+__device__ __forceinline__ uint64_t add64_fma(uint64_t a, uint64_t b, uint32_t one) {
+    uint64_t t;
+    uint32_t tl, th;
+    asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(t) : "r"(static_cast<uint32_t>(a)), "r"(one), "l"(b));
+    asm("mov.b64 {%0, %1}, %2;" : "=r"(tl), "=r"(th) : "l"(t));
+    asm("mad.lo.u32 %0, %1, %2, %0;" : "+r"(th) : "r"(static_cast<uint32_t>(a >> 32)), "r"(one));
+    asm("mov.b64 %0, {%1, %2};" : "=l"(t) : "r"(tl), "r"(th));
+    return t;
+}
+
+template <int CF, int AF>
+struct V {
+    uint32_t one;
+    __device__ __forceinline__ uint64_t addc(int which, uint64_t c, uint64_t d) const {
+        return (which < CF) ? add64_fma(d, c, one) : c + d;
+    }
+    __device__ __forceinline__ uint64_t adda(int which, uint64_t a, uint64_t b, uint64_t m) const {
+        return (which < AF) ? add64_fma(add64_fma(m, b, one), a, one) : a + b + m;
+    }
+#define VG(a, b, c, d, x, y)                                     \
+    a = adda(0, a, b, (x)); d = snt::Blake2b::ror32(d ^ a);      \
+    c = addc(0, c, d);      b = snt::Blake2b::ror24(b ^ c);      \
+    a = adda(1, a, b, (y)); d = snt::Blake2b::ror16(d ^ a);      \
+    c = addc(1, c, d);      b = snt::Blake2b::ror63(b ^ c);
+    __device__ __forceinline__ void compress(uint64_t h[8], const uint64_t m[16], uint64_t t, bool last) const {
+        const uint8_t S[12][16] = {
+            {0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15},
+            {14, 10, 4, 8, 9, 15, 13, 6, 1, 12, 0, 2, 11, 7, 5, 3},
+            {11, 8, 12, 0, 5, 2, 15, 13, 10, 14, 3, 6, 7, 1, 9, 4},
+            {7, 9, 3, 1, 13, 12, 11, 14, 2, 6, 5, 10, 4, 0, 15, 8},
+            {9, 0, 5, 7, 2, 4, 10, 15, 14, 1, 11, 12, 6, 8, 3, 13},
+            {2, 12, 6, 10, 0, 11, 8, 3, 4, 13, 7, 5, 15, 14, 1, 9},
+            {12, 5, 1, 15, 14, 13, 4, 10, 0, 7, 6, 3, 9, 2, 8, 11},
+            {13, 11, 7, 14, 12, 1, 3, 9, 5, 0, 15, 4, 8, 6, 2, 10},
+            {6, 15, 14, 9, 11, 3, 0, 8, 12, 2, 13, 7, 1, 4, 10, 5},
+            {10, 2, 8, 4, 7, 6, 1, 5, 15, 11, 9, 14, 3, 12, 13, 0},
+            {0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15},
+            {14, 10, 4, 8, 9, 15, 13, 6, 1, 12, 0, 2, 11, 7, 5, 3}};
+        uint64_t v0 = h[0], v1 = h[1], v2 = h[2], v3 = h[3], v4 = h[4], v5 = h[5], v6 = h[6], v7 = h[7];
+        uint64_t v8 = SNT_B2B_IV0, v9 = SNT_B2B_IV1, v10 = SNT_B2B_IV2, v11 = SNT_B2B_IV3;
+        uint64_t v12 = SNT_B2B_IV4 ^ t, v13 = SNT_B2B_IV5;
+        uint64_t v14 = last ? ~SNT_B2B_IV6 : SNT_B2B_IV6, v15 = SNT_B2B_IV7;
+#pragma unroll
+        for (int r = 0; r < 12; ++r) {
+            VG(v0, v4, v8, v12, m[S[r][0]], m[S[r][1]]);
+            VG(v1, v5, v9, v13, m[S[r][2]], m[S[r][3]]);
+            VG(v2, v6, v10, v14, m[S[r][4]], m[S[r][5]]);
+            VG(v3, v7, v11, v15, m[S[r][6]], m[S[r][7]]);
+            VG(v0, v5, v10, v15, m[S[r][8]], m[S[r][9]]);
+            VG(v1, v6, v11, v12, m[S[r][10]], m[S[r][11]]);
+            VG(v2, v7, v8, v13, m[S[r][12]], m[S[r][13]]);
+            VG(v3, v4, v9, v14, m[S[r][14]], m[S[r][15]]);
+        }
+        h[0] ^= v0 ^ v8;  h[1] ^= v1 ^ v9;  h[2] ^= v2 ^ v10; h[3] ^= v3 ^ v11;
+        h[4] ^= v4 ^ v12; h[5] ^= v5 ^ v13; h[6] ^= v6 ^ v14; h[7] ^= v7 ^ v15;
+    }
+};
+
+template <int CF, int AF>
+__global__ void __launch_bounds__(128) variant_kernel(uint32_t* out, int iters, uint32_t seed, uint32_t one, int check) {
+    V<CF, AF> v{one};
+    uint64_t h[8], m[16];
+    snt::Blake2b::init(h);
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) m[i] = h[i & 7] ^ (static_cast<uint64_t>(seed + i + threadIdx.x * 977u) << 13) ^ it;
+        v.compress(h, m, 128ull * (it + 1), false);
+    }
+    if (check) {
+        uint64_t r = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) r ^= h[i] * (2 * i + 1);
+        out[blockIdx.x * 128 + threadIdx.x] = static_cast<uint32_t>(r) ^ static_cast<uint32_t>(r >> 32);
+    } else if (h[0] == 0x12345678ull) {
+        out[blockIdx.x * 128 + threadIdx.x] = static_cast<uint32_t>(h[1]);
+    }
+}
+
+static uint32_t* g_out;
+static uint32_t* g_ref;
+
+template <int CF, int AF>
+static void run(int sms, int ctas_per_sm) {
+    const int g = sms * ctas_per_sm, it = 128;
+    variant_kernel<CF, AF><<<4, 128>>>(g_out, 3, 99u, 1u, 1);
+    CHECK(cudaDeviceSynchronize());
+    uint32_t a[512], b[512];
+    CHECK(cudaMemcpy(a, g_out, sizeof(a), cudaMemcpyDeviceToHost));
+    CHECK(cudaMemcpy(b, g_ref, sizeof(b), cudaMemcpyDeviceToHost));
+    int ok = 1;
+    for (int i = 0; i < 512; ++i) ok &= (a[i] == b[i]);
+    cudaEvent_t e0, e1;
+    CHECK(cudaEventCreate(&e0));
+    CHECK(cudaEventCreate(&e1));
+    float best = 1e30f;
+    for (int r = 0; r < 6; ++r) {
+        CHECK(cudaEventRecord(e0));
+        variant_kernel<CF, AF><<<g, 128>>>(g_out, it, 7u, 1u, 0);
+        CHECK(cudaEventRecord(e1));
+        CHECK(cudaEventSynchronize(e1));
+        float ms;
+        CHECK(cudaEventElapsedTime(&ms, e0, e1));
+        if (r > 0 && ms < best) best = ms;
+    }
+    CHECK(cudaGetLastError());
+    const double comp = double(g) * 128 * it;
+    printf("{\"c_adds_fma\": %d, \"a_adds_fma\": %d, \"warps_per_sm\": %d, \"ok\": %d, \"gbs\": %.1f}\n", CF, AF,
+           ctas_per_sm * 4, ok, comp * 128 / (best * 1e-3) / 1e9);
+}
+
+int main(int argc, char** argv) {
+    cudaDeviceProp prop;
+    CHECK(cudaGetDeviceProperties(&prop, 0));
+    const int sms = prop.multiProcessorCount;
+    CHECK(cudaMalloc(&g_out, sizeof(uint32_t) * sms * 16 * 128));
+    CHECK(cudaMalloc(&g_ref, sizeof(uint32_t) * 512));
+    variant_kernel<0, 0><<<4, 128>>>(g_ref, 3, 99u, 1u, 1);
+    CHECK(cudaDeviceSynchronize());
+    if (argc > 2) {      // one variant only (for ncu): blake2b_variants <cf> <af> [ctas_per_sm]
+        const int cf = atoi(argv[1]), af = atoi(argv[2]), occ = argc > 3 ? atoi(argv[3]) : 4;
+        if (cf == 0 && af == 0) run<0, 0>(sms, occ);
+        else if (cf == 2 && af == 0) run<2, 0>(sms, occ);
+        else if (cf == 2 && af == 1) run<2, 1>(sms, occ);
+        else { fprintf(stderr, "variant not instantiated\n"); return 2; }
+        return 0;
+    }
+    for (int occ : {2, 4}) {
+        run<0, 0>(sms, occ);
+        run<1, 0>(sms, occ);
+        run<2, 0>(sms, occ);
+        run<2, 1>(sms, occ);
+        run<2, 2>(sms, occ);
+        run<1, 1>(sms, occ);
+        run<0, 1>(sms, occ);
+    }
+    return 0;
+}

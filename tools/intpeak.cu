@@ -6,7 +6,9 @@
 //     IMAD on the FMA pipe) with 8 independent dependency chains per thread,
 //   * an ALU+FMA mix (can adds ride on the FMA pipe while logic saturates ALU?),
 //   * the three compression functions fed from registers (no memory traffic):
-//     the compute-only ceiling of the leaf kernels.
+//     the compute-only ceiling of the leaf kernels (SHA-256 both as the compiler
+//     places it -- additions on the ALU pipe -- and in the product's formulation
+//     with every addition an IMAD on the FMA pipe).
 // Output: one JSON object on stdout. Rates are in 10^12 thread-instructions/s
 // ("Tops/s") over the whole GPU at the clocks the run saw.
 #include <cuda_runtime.h>
@@ -116,6 +118,20 @@ __global__ void __launch_bounds__(128) sha256_kernel(uint32_t* out, int iters, u
     if (s[0] == 0x12345678u) out[blockIdx.x * 128 + threadIdx.x] = s[1];
 }
 
+// the product's formulation: every addition an IMAD with at most two vector operands (sha256.cuh)
+__constant__ uint32_t k_ones[32] = {1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1};
+__global__ void __launch_bounds__(128) sha256_fma_kernel(uint32_t* out, int iters, uint32_t seed, uint32_t one) {
+    uint32_t s[8], w[16];
+    snt::Sha256::init(s);
+    const snt::Sha256::One o(one, k_ones[threadIdx.x & 31]);
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) w[i] = s[i & 7] ^ (seed + i + it + threadIdx.x * 977u);
+        snt::Sha256::compress(s, w, o);
+    }
+    if (s[0] == 0x12345678u) out[blockIdx.x * 128 + threadIdx.x] = s[1];
+}
+
 __global__ void __launch_bounds__(128) blake2b_kernel(uint32_t* out, int iters, uint32_t seed) {
     uint64_t h[8], m[16];
     snt::Blake2b::init(h);
@@ -200,6 +216,9 @@ int main() {
         float ms = time_ms([&] { sha256_kernel<<<g, 128>>>(out, it, 7u); }, 5);
         double comp = double(g) * 128 * it;
         printf(", \"sha256_regs_gcomp_s\": %.3f, \"sha256_regs_gbs\": %.1f", comp / (ms * 1e-3) / 1e9,
+               comp * 64 / (ms * 1e-3) / 1e9);
+        ms = time_ms([&] { sha256_fma_kernel<<<g, 128>>>(out, it, 7u, 1u); }, 5);
+        printf(", \"sha256_fma_regs_gcomp_s\": %.3f, \"sha256_fma_regs_gbs\": %.1f", comp / (ms * 1e-3) / 1e9,
                comp * 64 / (ms * 1e-3) / 1e9);
         ms = time_ms([&] { blake2b_kernel<<<g, 128>>>(out, it, 7u); }, 5);
         printf(", \"blake2b_regs_gcomp_s\": %.3f, \"blake2b_regs_gbs\": %.1f", comp / (ms * 1e-3) / 1e9,
