@@ -270,3 +270,61 @@ def digest_dataset(manifest: DatasetManifest, batch_size: int = 128, shuffle_see
     acc = _dev.LatticeAccumulator(len(source_ids))
     ds.accumulate(acc)
     return _finalize_device(acc, ds.source_ids)
+
+
+class StreamingDatasetHasher:
+    """Per-source LtHash folded into a training loop, batch by batch, with no host round trip.
+
+    The reference's loader-side protocol is ``process_batch(batch, acc)`` over host records
+    (dataset.py:74-86, the on-the-fly use of PAPER.md:504-515). Here a batch is what a GPU data
+    loader already holds: a ``[B, ...]`` tensor of fixed-size samples (any dtype, CUDA or pinned
+    host memory) plus ``sample_ids`` and ``source_ids`` tensors. ``update`` maps source ids to
+    accumulator slots on the device, enqueues one ``snt_lthash_samples`` launch on the current
+    stream and returns at once; nothing is synchronised until ``finalize``. The result equals
+    ``digest_dataset`` over the same samples for any batch size and order.
+    """
+
+    def __init__(self, source_ids: Iterable[int]):
+        self._dev = _dev.require_cuda()
+        self.source_ids = sorted(set(int(s) for s in source_ids))
+        if not self.source_ids:
+            raise ValidationError("at least one declared source is required")
+        self._table = torch.tensor(self.source_ids, dtype=torch.int64, device=self._dev)
+        self._acc = _dev.LatticeAccumulator(len(self.source_ids))
+        self._rows: Dict[Tuple[int, int], Tuple[torch.Tensor, torch.Tensor]] = {}   # (B, row bytes) -> offsets, lengths
+
+    def _row_index(self, n: int, row_bytes: int) -> Tuple[torch.Tensor, torch.Tensor]:
+        key = (n, row_bytes)
+        if key not in self._rows:
+            off = torch.arange(n, dtype=torch.int64, device=self._dev) * row_bytes
+            self._rows[key] = (off, torch.full((n,), row_bytes, dtype=torch.int64, device=self._dev))
+        return self._rows[key]
+
+    def update(self, data: torch.Tensor, sample_ids, source_ids) -> None:
+        """Fold one batch in: row i of ``data`` is sample ``sample_ids[i]`` of source ``source_ids[i]``."""
+        if data.dim() < 1 or data.shape[0] == 0:
+            return
+        n = int(data.shape[0])
+        flat = _dev.as_device_bytes(data, self._dev)
+        row_bytes = flat.numel() // n
+        off, ln = self._row_index(n, row_bytes)
+        ids = torch.as_tensor(sample_ids).to(self._dev, dtype=torch.int64, non_blocking=True).reshape(-1)
+        src = torch.as_tensor(source_ids).to(self._dev, dtype=torch.int64, non_blocking=True).reshape(-1)
+        if ids.numel() != n or src.numel() != n:
+            raise ValidationError("sample_ids and source_ids need one entry per row of the batch")
+        pos = torch.searchsorted(self._table, src).clamp_(max=len(self.source_ids) - 1)
+        # an undeclared source gets slot n_sources: the kernel flags it in the status word (checked in finalize)
+        slots = torch.where(self._table[pos] == src, pos, torch.full_like(pos, len(self.source_ids))).to(torch.int32)
+        if flat.numel() == 0:
+            flat = torch.zeros(16, dtype=torch.uint8, device=self._dev)
+        self._acc.add_samples(flat, off, ln, ids, slots)
+
+    def finalize(self) -> Dict[int, Tuple[LatticeDigest, int]]:
+        """Per-source digests and counts, ordered by source id; raises if any batch named an undeclared source."""
+        return _finalize_device(self._acc, self.source_ids)
+
+    def allreduce(self, group=None) -> None:
+        """Combine the per-rank sums of a data-parallel job (one all-reduce, see distributed.py)."""
+        from . import distributed as _dd
+
+        _dd.allreduce_lattice(self._acc.acc, self._acc.counts, self._acc.status, group)

@@ -161,6 +161,22 @@ class MerkleModelHasher:
                                     _ptr(self.out), _stream())
         _native.check(rc, "snt_merkle_inplace")
 
+    def capture(self) -> "torch.cuda.CUDAGraph":
+        """Record ``run`` (leaf launch + level-reducer launches) into a CUDA graph.
+
+        ``graph.replay()`` then re-hashes whatever bytes the tensors hold at replay time into
+        ``self.out`` with one submission instead of three launches -- for callers that re-hash
+        the same model every few steps (small models are launch-latency sensitive: GPT-2 small
+        is one wave of CTAs). The first ``run`` happens outside the capture so that one-time
+        function-attribute calls are not recorded.
+        """
+        self.run()
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            self.run()
+        return graph
+
     def run_leaves_only(self, begin: Optional[int] = None, end: Optional[int] = None) -> None:
         """The leaf stage alone (``snt_merkle_leaves``) over [begin, end) of this hasher's range."""
         lib = _native.load()

@@ -29,6 +29,7 @@ from .errors import InvalidInput
 from .workers import chunk_ranges
 
 DEFAULT_SHARD_LEVELS = 10   # 1024 leaves = 8 MiB of tensor bytes per shard
+STATUS_BITS = 4             # flag bits of LatticeAccumulator.status carried through the all-reduce
 
 
 def ceil_div(a: int, b: int) -> int:
@@ -206,17 +207,32 @@ def sample_ranges(n_samples: int, world: int) -> List[Tuple[int, int]]:
 
 def allreduce_lattice(acc: torch.Tensor, counts: torch.Tensor, status: Optional[torch.Tensor] = None,
                       group=None) -> None:
-    """Sum the widened lane accumulators and counts over all ranks, in place.
+    """Sum the widened lane accumulators and counts over all ranks, in place, with ONE all-reduce.
 
-    ``acc`` is int32 (the bit pattern of u32 lanes; two's-complement addition is
-    the same sum modulo 2^32), ``counts`` int64. One all-reduce each, latency bound.
+    ``acc`` is int32 (the bit pattern of u32 lanes), ``counts`` int64, ``status`` an int32 flag word.
+    The three are packed into one int64 buffer -- lanes zero-extended, the status flag as 0/1 -- so a
+    single ``all_reduce(SUM)`` of ``n_sources * 33 + STATUS_BITS`` words carries everything (a lane sum modulo
+    2^64 truncated to 32 bits is the sum modulo 2^32, hence still exact modulo 2^16; a summed flag is
+    non-zero exactly when some rank raised it; each of the STATUS_BITS flag bits travels as its own
+    word so the result is the OR of the ranks' flag words). The message is a few KB: latency bound, which is why
+    it is one collective and not three.
     """
-    for t, op in ((acc, dist.ReduceOp.SUM), (counts, dist.ReduceOp.SUM), (status, dist.ReduceOp.MAX)):
-        if t is None:
-            continue
-        if _needs_host_staging(t, group):
-            host = t.cpu()
-            dist.all_reduce(host, op=op, group=group)
-            t.copy_(host)
-        else:
-            dist.all_reduce(t, op=op, group=group)
+    n_acc, n_cnt = acc.numel(), counts.numel()
+    packed = torch.zeros(n_acc + n_cnt + STATUS_BITS, dtype=torch.int64, device=acc.device)
+    packed[:n_acc] = acc.to(torch.int64) & 0xFFFFFFFF
+    packed[n_acc:n_acc + n_cnt] = counts
+    if status is not None:
+        bits = torch.arange(STATUS_BITS, device=acc.device, dtype=torch.int64)
+        packed[n_acc + n_cnt:] = (status.reshape(-1)[:1].to(torch.int64) >> bits) & 1
+    if _needs_host_staging(packed, group):
+        host = packed.cpu()
+        dist.all_reduce(host, op=dist.ReduceOp.SUM, group=group)
+        packed.copy_(host)
+    else:
+        dist.all_reduce(packed, op=dist.ReduceOp.SUM, group=group)
+    low = packed[:n_acc] & 0xFFFFFFFF
+    acc.copy_((((low + 0x80000000) & 0xFFFFFFFF) - 0x80000000).to(torch.int32))   # u32 bit pattern as int32
+    counts.copy_(packed[n_acc:n_acc + n_cnt])
+    if status is not None:
+        bits = torch.arange(STATUS_BITS, device=acc.device, dtype=torch.int64)
+        status.copy_((((packed[n_acc + n_cnt:] != 0).to(torch.int64) << bits).sum()).to(status.dtype).reshape(1))

@@ -102,7 +102,9 @@ def _lattice_worker(rank, world, port, q):
         acc[0, 0] += np.uint32(0xFFFF0000)          # force a wrap modulo 2^32 in the all-reduce on one lane
         t_acc = torch.from_numpy(acc.view(np.int32).reshape(-1).copy())
         t_cnt = torch.from_numpy(counts.copy())
-        dd.allreduce_lattice(t_acc, t_cnt)
+        t_status = torch.tensor([1 if rank == 1 else 4], dtype=torch.int32)   # flag words are OR-ed
+        dd.allreduce_lattice(t_acc, t_cnt, t_status)
+        assert int(t_status.item()) == 5
         got = (t_acc.numpy().view(np.uint32).reshape(len(sources), 32) & 0xFFFF).astype("<u2")
         want = orc.dataset_digests(samples, declared=sources)
         ok = all(got[i].tobytes() == want[s][0] and int(t_cnt[i]) == want[s][1] for i, s in enumerate(sources))

@@ -580,3 +580,55 @@ def test_sign_and_verify_gpu_digests_end_to_end(pkg):
     tampered = pkg.TensorMap([(n, (b[:-1] + bytes([b[-1] ^ 1])) if n == "l2" else b) for n, b in model.entries])
     bad = pkg.hash_model(replay, tampered)
     assert pkg.verify_bundle(bundle, {"m": {cfg.alg.value: bad.digest_hex()}}) is pkg.Verdict.DIGEST_MISMATCH
+
+
+# ---- streaming loader hook, CUDA-graph replay --------------------------------------------------
+
+def test_streaming_hasher_equals_whole_dataset_pass(pkg, porc):
+    """Batches of a [N, 3, 8, 8] uint8 tensor in shuffled order == one pass == the oracle."""
+    from paper_2510_00554_b200 import dataset as dsm
+
+    n, n_src = 1000, 7
+    rng = np.random.default_rng(5)
+    data = rng.integers(0, 256, size=(n, 3, 8, 8), dtype=np.uint8)
+    ids = rng.permutation(n).astype(np.int64) + 10_000
+    declared = [3, 4, 8, 15, 16, 23, 42]
+    src = np.array(declared)[rng.integers(0, n_src, size=n)]
+    want = porc.dataset_digests([(int(ids[i]), int(src[i]), b"", data[i].tobytes()) for i in range(n)],
+                                declared=declared)
+    order = rng.permutation(n)
+    for batch in (1, 128, 333):
+        h = dsm.StreamingDatasetHasher(declared)
+        dev_data = torch.from_numpy(data).cuda()
+        for s in range(0, n, batch):
+            idx = order[s:s + batch]
+            rows = dev_data[torch.from_numpy(idx).cuda()] if batch != 128 else torch.from_numpy(data[idx])  # CUDA and host batches
+            h.update(rows, torch.from_numpy(ids[idx]), torch.from_numpy(src[idx]))
+        got = h.finalize()
+        assert {k: (v[0].data, v[1]) for k, v in got.items()} == {k: (v[0], v[1]) for k, v in want.items()}
+
+
+def test_streaming_hasher_flags_undeclared_source(pkg):
+    from paper_2510_00554_b200 import dataset as dsm
+    from paper_2510_00554_b200.errors import ValidationError
+
+    h = dsm.StreamingDatasetHasher([1, 2])
+    h.update(torch.zeros(4, 16, dtype=torch.float32), torch.arange(4), torch.tensor([1, 2, 5, 1]))
+    with pytest.raises(ValidationError):
+        h.finalize()
+
+
+def test_graph_replay_rehashes_current_bytes(pkg, porc):
+    from paper_2510_00554_b200 import device as dev
+
+    tensors = inputs.model_tensors(77, [8192 * 300 + 5, 100, 8192 * 64, 0, 70001])
+    dts = [dev.as_device_bytes(t) for t in tensors]
+    plan = dev.ModelPlan(dts, 8192)
+    hasher = dev.MerkleModelHasher(plan, "sha256")
+    graph = hasher.capture()
+    graph.replay()
+    assert hasher.out_bytes() == porc.inplace_merkle("sha256", tensors, 8192)
+    dts[0][12345] ^= 0x40                                   # the model changes in place ...
+    changed = [bytes(dts[0].cpu().numpy().tobytes())] + tensors[1:]
+    graph.replay()                                          # ... and the same graph hashes the new bytes
+    assert hasher.out_bytes() == porc.inplace_merkle("sha256", changed, 8192)

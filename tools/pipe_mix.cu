@@ -99,7 +99,48 @@ __global__ void __launch_bounds__(THREADS) regs_kernel(uint32_t* out, int iters,
     if (r == 0x12345678u) out[blockIdx.x * THREADS + threadIdx.x] = r;
 }
 
+// Does a warp instruction cost less when only half of the warp's lanes are active? `active` lanes per
+// warp run a pure ALU (SHF) loop; the rest exit at once. Rate is reported per *warp instruction*.
+template <int THREADS>
+__global__ void __launch_bounds__(THREADS) lanes_kernel(uint32_t* out, int iters, uint32_t seed, int active) {
+    if (static_cast<int>(threadIdx.x & 31) >= active) return;
+    uint32_t x[CHAINS];
+#pragma unroll
+    for (int c = 0; c < CHAINS; ++c) x[c] = seed + c * 0x9e3779b9u + threadIdx.x;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int r = 0; r < 64; ++r) asm volatile("shf.r.wrap.b32 %0, %0, %0, 7;" : "+r"(x[r % CHAINS]));
+    }
+    uint32_t r = 0;
+#pragma unroll
+    for (int c = 0; c < CHAINS; ++c) r ^= x[c];
+    if (r == 0x12345678u) out[blockIdx.x * THREADS + threadIdx.x] = r;
+}
+
 static uint32_t* g_out;
+
+static void run_lanes(int sms, int warps_per_sm, int active) {
+    constexpr int THREADS = 128;
+    const int grid = sms * (warps_per_sm / 4);
+    const int iters = 400;
+    cudaEvent_t a, b;
+    CHECK(cudaEventCreate(&a));
+    CHECK(cudaEventCreate(&b));
+    float best = 1e30f;
+    for (int r = 0; r < 5; ++r) {
+        CHECK(cudaEventRecord(a));
+        lanes_kernel<THREADS><<<grid, THREADS>>>(g_out, iters, 12345u, active);
+        CHECK(cudaEventRecord(b));
+        CHECK(cudaEventSynchronize(b));
+        float ms;
+        CHECK(cudaEventElapsedTime(&ms, a, b));
+        if (r > 0 && ms < best) best = ms;
+    }
+    CHECK(cudaGetLastError());
+    const double warp_instr = double(grid) * (THREADS / 32) * double(iters) * 64;
+    printf("{\"active_lanes\": %d, \"warps_per_sm\": %d, \"warp_instr_per_clk_per_smsp\": %.4f}\n", active, warps_per_sm,
+           warp_instr / (best * 1e-3) / (sms * 4.0) / 1.965e9);
+}
 
 template <int AR, int FR>
 static void run_regs(int sms, int warps_per_sm) {
@@ -156,6 +197,7 @@ int main() {
     CHECK(cudaGetDeviceProperties(&prop, 0));
     const int sms = prop.multiProcessorCount;
     CHECK(cudaMalloc(&g_out, sizeof(uint32_t) * sms * 32 * 128));
+    for (int act : {32, 24, 16, 8}) run_lanes(sms, 32, act);
     for (int w : {32, 64}) {
         run_regs<1, 0>(sms, w); run_regs<2, 0>(sms, w); run_regs<3, 0>(sms, w);
         run_regs<0, 1>(sms, w); run_regs<0, 2>(sms, w); run_regs<0, 3>(sms, w);
