@@ -67,6 +67,8 @@ __device__ __forceinline__ void to_words(const U4& q0, const U4& q1, const U4& q
 }
 
 // THREADS per CTA, MINB = min CTAs per SM (register cap), IMAD = schedule adds on FMA pipe,
+__constant__ uint32_t k_ones[32] = {1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1};
+
 // WIDE = 128 bytes per thread per iteration, HINT = load flavour
 template <int THREADS, int MINB, int IMAD, int WIDE, int HINT>
 __global__ void __launch_bounds__(THREADS, MINB)
@@ -75,7 +77,9 @@ leaf_kernel(const uint8_t* __restrict__ data, uint64_t n_leaves, const __grid_co
     const uint64_t k = static_cast<uint64_t>(blockIdx.x) * THREADS + threadIdx.x;
     if (k >= n_leaves) return;
     const uint8_t* p = data + (k << 13);
-    const uint32_t one = IMAD ? prm.one : 1u;
+    // IMAD = 1: the product's formulation (every addition an IMAD, sha256.cuh); 0: compile-time ones, i.e.
+    // the additions fold back to ALU-pipe IADD3 (the stock placement)
+    const Sha256::One one = IMAD ? Sha256::One(prm.one, k_ones[threadIdx.x & 31]) : Sha256::One();
     uint32_t s[8];
     Sha256::init(s);
     if (!WIDE) {
@@ -108,7 +112,7 @@ leaf_kernel(const uint8_t* __restrict__ data, uint64_t n_leaves, const __grid_co
             Sha256::compress(s, w2, one);
         }
     }
-    Sha256::compress_const(s, prm.pad_kw);
+    Sha256::compress_const(s, prm.pad_kw, one);
     uint4* o = reinterpret_cast<uint4*>(out + k * 32);
     o[0] = make_uint4(bswap32(s[0]), bswap32(s[1]), bswap32(s[2]), bswap32(s[3]));
     o[1] = make_uint4(bswap32(s[4]), bswap32(s[5]), bswap32(s[6]), bswap32(s[7]));
