@@ -71,6 +71,30 @@ def as_device_bytes(buf, device: Optional[torch.device] = None) -> torch.Tensor:
     return host.to(device, non_blocking=True)
 
 
+def device_spans(buffers: Sequence[object], device: Optional[torch.device] = None):
+    """(keep-alive list, addresses, byte lengths) of the buffers' bytes in HBM, in order.
+
+    The fast path of the drop-in API: a contiguous CUDA tensor is described by its
+    ``data_ptr()`` and ``nbytes`` alone -- no detach / reshape / view per tensor, which for a
+    581-tensor state dict costs more host time than a GPT-2 small hash takes on the GPU.
+    Anything else (host memory, non-contiguous tensors) is staged through ``as_device_bytes``.
+    """
+    device = device or require_cuda()
+    n = len(buffers)
+    keep: List[object] = [None] * n
+    ptrs = np.zeros(max(n, 1), dtype=np.uint64)
+    sizes = np.zeros(max(n, 1), dtype=np.uint64)
+    for i, buf in enumerate(buffers):
+        if not (type(buf) is torch.Tensor and buf.is_cuda and buf.is_contiguous()):
+            buf = as_device_bytes(buf, device)
+        nbytes = buf.nbytes
+        keep[i] = buf
+        sizes[i] = nbytes
+        if nbytes:
+            ptrs[i] = buf.data_ptr()
+    return keep, ptrs, sizes
+
+
 class ModelPlan:
     """Device-side block table over fragmented tensors (``snt_model_plan``).
 
@@ -100,6 +124,23 @@ class ModelPlan:
         self.block_size = block_size
         self.leaf_count = int(lib.snt_model_plan_leaf_count(self._handle))
         self.total_bytes = int(lib.snt_model_plan_total_bytes(self._handle))
+
+    @classmethod
+    def from_spans(cls, keep: Sequence[object], ptrs: np.ndarray, sizes: np.ndarray, block_size: int) -> "ModelPlan":
+        """Plan over ``device_spans`` output (addresses + byte lengths; ``keep`` holds the owners alive)."""
+        self = cls.__new__(cls)
+        self._handle = ctypes.c_void_p()
+        lib = _native.load()
+        require_cuda()
+        self.tensors = list(keep)
+        rc = lib.snt_model_plan_create(ptrs.ctypes.data_as(ctypes.POINTER(ctypes.c_void_p)),
+                                       sizes.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), len(keep), block_size,
+                                       _stream(), ctypes.byref(self._handle))
+        _native.check(rc, "snt_model_plan_create")
+        self.block_size = block_size
+        self.leaf_count = int(lib.snt_model_plan_leaf_count(self._handle))
+        self.total_bytes = int(lib.snt_model_plan_total_bytes(self._handle))
+        return self
 
     @property
     def handle(self) -> ctypes.c_void_p:

@@ -267,11 +267,15 @@ def _inplace_merkle_staged(cfg: HashConfig, model: TensorMap) -> ModelDigestResu
 
 def inplace_hash(cfg: HashConfig, model: TensorMap, workers: int = 1) -> ModelDigestResult:
     """Hash fragmented tensors where they lie: no copy, no padding (model.py:298-315)."""
-    _require_nonempty(model)
-    host_bytes = sum(buffer_nbytes(buf) for _, buf in model.entries if not _is_cuda(buf))
-    if cfg.construction is Construction.MERKLE and host_bytes >= STAGE_PIPELINE_MIN_BYTES:
-        return _inplace_merkle_staged(cfg, model)
-    plan = _dev.ModelPlan(device_tensors(model), cfg.block_size)
+    buffers = [buf for _, buf in model.entries]
+    all_resident = all(type(buf) is torch.Tensor and buf.is_cuda for buf in buffers)
+    if not all_resident:
+        _require_nonempty(model)
+        host_bytes = sum(buffer_nbytes(buf) for buf in buffers if not _is_cuda(buf))
+        if cfg.construction is Construction.MERKLE and host_bytes >= STAGE_PIPELINE_MIN_BYTES:
+            return _inplace_merkle_staged(cfg, model)
+    # an empty model is rejected by snt_model_plan_create (InvalidInput, model.py:166-168)
+    plan = _dev.ModelPlan.from_spans(*_dev.device_spans(buffers), cfg.block_size)
     try:
         return _hash_plan(cfg, plan)
     finally:
