@@ -98,36 +98,41 @@ class DeviceDataset:
 
     @classmethod
     def from_host(cls, shard, offsets, lengths, ids, source_of_sample, source_ids: Sequence[int],
-                  pinned: bool = False) -> "DeviceDataset":
-        """Copy host arrays to the device. ``source_of_sample`` holds source ids, not slots."""
+                  pinned: bool = True) -> "DeviceDataset":
+        """Copy host arrays to the device. ``source_of_sample`` holds source ids, not slots.
+
+        The shard copy is enqueued first (asynchronous when the shard is pinned) so that the
+        host-side slot mapping overlaps it; the four row arrays then travel as ONE packed,
+        pinned buffer (3 x u64 + 1 x u32 per sample) instead of four pageable copies.
+        """
         dev = _dev.require_cuda()
+        shard_t = _dev.as_device_bytes(shard, dev)
+        if shard_t.numel() == 0:
+            shard_t = torch.zeros(16, dtype=torch.uint8, device=dev)
         source_ids = sorted(set(int(s) for s in source_ids))
         src = np.asarray(source_of_sample, dtype=np.int64)
+        n = int(src.shape[0])
         table = np.asarray(source_ids, dtype=np.int64)
         slots = np.searchsorted(table, src)
         if table.size:
             hit = table[np.minimum(slots, table.size - 1)] == src
         else:
             hit = np.zeros(src.shape, dtype=bool)
-        slots = np.where(hit, slots, -1)
-        bad = np.nonzero(slots < 0)[0]
-        if bad.size:
-            i = int(bad[0])
+        if not hit.all():
+            i = int(np.nonzero(~hit)[0][0])
             raise ValidationError(f"sample {int(np.asarray(ids)[i])} references undeclared source {int(src[i])}")
 
-        def up(a, dtype):
-            t = torch.from_numpy(np.ascontiguousarray(np.asarray(a).astype(dtype, copy=False)))
-            if pinned:
-                t = t.pin_memory()
-            return t.to(dev, non_blocking=True)
-
-        shard_t = _dev.as_device_bytes(shard, dev)
-        if shard_t.numel() == 0:
-            shard_t = torch.zeros(16, dtype=torch.uint8, device=dev)
-        return cls(shard_t, up(np.asarray(offsets, dtype=np.uint64).view(np.int64), np.int64),
-                   up(np.asarray(lengths, dtype=np.uint64).view(np.int64), np.int64),
-                   up(np.asarray(ids, dtype=np.uint64).view(np.int64), np.int64),
-                   up(slots, np.int32), source_ids)
+        packed = torch.empty(max(n, 1) * 28, dtype=torch.uint8, pin_memory=True)
+        view = packed.numpy()
+        view[0:8 * n].view(np.uint64)[:] = np.asarray(offsets, dtype=np.uint64)
+        view[8 * n:16 * n].view(np.uint64)[:] = np.asarray(lengths, dtype=np.uint64)
+        view[16 * n:24 * n].view(np.uint64)[:] = np.asarray(ids, dtype=np.uint64)
+        view[24 * n:28 * n].view(np.int32)[:] = slots.astype(np.int32, copy=False)
+        rows = packed.to(dev, non_blocking=True)
+        ds = cls(shard_t, rows[0:8 * n].view(torch.int64), rows[8 * n:16 * n].view(torch.int64),
+                 rows[16 * n:24 * n].view(torch.int64), rows[24 * n:28 * n].view(torch.int32), source_ids)
+        ds._staging = packed      # the pinned staging block outlives the asynchronous copy
+        return ds
 
     def accumulate(self, acc: "_dev.LatticeAccumulator", begin: int = 0, end: Optional[int] = None,
                    digests: Optional[torch.Tensor] = None) -> None:
