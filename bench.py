@@ -289,7 +289,9 @@ def run_ours(args):
     prof = ROOT / "profiles" / "ncu_traffic.json"
     if prof.exists():
         try:
-            roofline["traffic"] = json.loads(prof.read_text()).get(f"merkle_leaf_kernel<{args.alg}>:{args.arch}")
+            whole = json.loads(prof.read_text()).get(f"merkle_leaf_kernel<{args.alg}>:{args.arch}")
+            # per launch, like `achieved`: a rank's launch covers its share of the leaves
+            roofline["traffic"] = whole if (whole is None or world == 1) else int(whole * my_leaves / n_leaves)
         except Exception:
             pass
 

@@ -176,7 +176,9 @@ class MerkleModelHasher:
     """
 
     def __init__(self, plan: ModelPlan, alg: str, leaf_begin: int = 0, leaf_end: Optional[int] = None,
-                 levels: Optional[int] = None):
+                 levels: Optional[int] = None, out_capacity: Optional[int] = None):
+        """``out_capacity`` (in digests) over-allocates the zero-filled output buffer so that a rank's
+        shard roots can be handed to an all-gather of fixed-size slots without a staging copy."""
         self.plan = plan
         self.alg = alg
         self.dlen = DIGEST_LEN[alg]
@@ -192,7 +194,8 @@ class MerkleModelHasher:
         self.leaves = torch.empty(count * self.dlen, dtype=torch.uint8, device=dev)
         self.work_bytes = merkle_work_bytes(alg, count)
         self.work = torch.empty(max(self.work_bytes, 16), dtype=torch.uint8, device=dev)
-        self.out = torch.empty(self.n_out * self.dlen, dtype=torch.uint8, device=dev)
+        self.out_padded = torch.zeros(max(self.n_out, out_capacity or 0) * self.dlen, dtype=torch.uint8, device=dev)
+        self.out = self.out_padded[:self.n_out * self.dlen]
 
     def run(self) -> None:
         lib = _native.load()

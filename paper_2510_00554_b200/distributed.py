@@ -98,6 +98,28 @@ class CudaBackend:
         h.run()
         return h.out
 
+    def shard_roots_padded(self, leaf_begin: int, leaf_end: int, levels: int, slots: int) -> torch.Tensor:
+        """Same, written at the front of a zero-filled buffer of ``slots`` digests (an all-gather slot)."""
+        key = (leaf_begin, leaf_end, levels, slots)
+        h = self._hashers.get(key)
+        if h is None:
+            h = self._dev.MerkleModelHasher(self.plan, self.alg, leaf_begin, leaf_end, levels, out_capacity=slots)
+            self._hashers[key] = h
+        h.run()
+        return h.out_padded
+
+    def gather_buffers(self, shard_plan: "ShardPlan", world: int, widest: int):
+        """Persistent receive buffer of the all-gather and the row index that compacts its slots
+        (rank r's first ``shard_count(r)`` rows) into shard order."""
+        key = ("gather", shard_plan.n_shards, world, widest)
+        got = self._hashers.get(key)
+        if got is None:
+            recv = torch.empty(world * widest * self.dlen, dtype=torch.uint8, device=self.device)
+            rows = [r * widest + i for r in range(world) for i in range(shard_plan.shard_count(r))]
+            got = (recv, torch.tensor(rows, dtype=torch.int64, device=self.device))
+            self._hashers[key] = got
+        return got
+
     def root_of(self, nodes: torch.Tensor, count: int) -> torch.Tensor:
         return self._dev.merkle_root_device(self.alg, nodes, count)
 
@@ -122,11 +144,26 @@ def sharded_merkle_root(backend, shard_plan: ShardPlan, rank: int, world: int, g
     dlen = backend.dlen
     begin, end = shard_plan.leaf_range(rank)
     mine = shard_plan.shard_count(rank)
-    local = backend.shard_roots(begin, end, shard_plan.levels) if mine else None
+    fused_slot = world > 1 and hasattr(backend, "shard_roots_padded")
+    local = backend.shard_roots(begin, end, shard_plan.levels) if (mine and not fused_slot) else None
     if world == 1:
         if shard_plan.n_shards == 1:
             return local                               # already the single level-k node = the root
         nodes = local
+    elif fused_slot:
+        # product path (NCCL): the leaf + shard-reduce launches write straight into the all-gather slot,
+        # the receive buffer is persistent, one index_select puts the roots in shard order
+        widest = max(shard_plan.shard_count(r) for r in range(world))
+        send = backend.shard_roots_padded(begin, end, shard_plan.levels, widest) if mine else \
+            torch.zeros(widest * dlen, dtype=torch.uint8, device=backend.device)
+        recv, rows = backend.gather_buffers(shard_plan, world, widest)
+        if _needs_host_staging(send, group):           # debugging over gloo: same buffers, staged through the host
+            host = torch.empty(recv.numel(), dtype=torch.uint8)
+            dist.all_gather_into_tensor(host, send.cpu(), group=group)
+            recv.copy_(host)
+        else:
+            dist.all_gather_into_tensor(recv, send, group=group)
+        nodes = recv.view(world * widest, dlen).index_select(0, rows).view(-1)
     else:
         widest = max(shard_plan.shard_count(r) for r in range(world))
         send = torch.zeros(widest * dlen, dtype=torch.uint8, device=backend.device)

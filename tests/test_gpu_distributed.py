@@ -1,0 +1,88 @@
+"""The multi-rank shard-and-combine path on real CUDA kernels: several ranks share the one GPU of
+the test box and talk over gloo (NCCL refuses two ranks on one device). Everything but the NCCL
+call itself is the product path: per-rank leaf ranges, shard roots written into the all-gather
+slot, index-compacted receive buffer, top reduce; packed lattice all-reduce.
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+import inputs
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, sizes, q):
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2510_00554_b200 as pkg
+        from paper_2510_00554_b200 import dataset as dsm, distributed as dd
+
+        torch.cuda.set_device(0)
+        tensors = inputs.model_tensors(91, sizes)
+        out = {}
+        for alg in ("sha256", "blake2b", "sha3-256"):
+            cfg = pkg.HashConfig(pkg.Construction.MERKLE, pkg.Strategy.IN_PLACE, pkg.CompressionAlg.from_name(alg))
+            # odd ranks hold the model on the GPU, even ranks as host bytes
+            entries = [(f"t{i}", torch.frombuffer(bytearray(t), dtype=torch.uint8).cuda() if (rank % 2 and t) else t)
+                       for i, t in enumerate(tensors)]
+            out[alg] = dd.hash_model_sharded(cfg, pkg.TensorMap(entries), rank, world).model_digest.data.hex()
+
+        n, declared = 999, [2, 3, 5, 7]
+        rng = np.random.default_rng(17)
+        data = rng.integers(0, 256, size=(n, 96), dtype=np.uint8)
+        ids = np.arange(n, dtype=np.int64) * 3 + 1
+        src = np.array(declared)[rng.integers(0, len(declared), size=n)]
+        a, b = dd.sample_ranges(n, world)[rank]
+        h = dsm.StreamingDatasetHasher(declared)
+        for s in range(a, b, 100):
+            e = min(b, s + 100)
+            h.update(torch.from_numpy(data[s:e]).cuda(), torch.from_numpy(ids[s:e]), torch.from_numpy(src[s:e]))
+        h.allreduce()
+        out["lattice"] = {k: (v[0].data.hex(), v[1]) for k, v in h.finalize().items()}
+        q.put((rank, out))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_ranks_sharing_the_gpu_reproduce_single_gpu_digests(world, porc):
+    import torch.multiprocessing as mp
+
+    sizes = [8192 * 1500 + 77, 100, 0, 8192 * 2100, 31, 8192 * 900 + 4096, 5000]     # 4,501+ leaves: 5 shards of 1024
+    tensors = inputs.model_tensors(91, sizes)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, sizes, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = dict(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(60)
+        assert p.exitcode == 0
+
+    n, declared = 999, [2, 3, 5, 7]
+    rng = np.random.default_rng(17)
+    data = rng.integers(0, 256, size=(n, 96), dtype=np.uint8)
+    ids = np.arange(n, dtype=np.int64) * 3 + 1
+    src = np.array(declared)[rng.integers(0, len(declared), size=n)]
+    want_lat = porc.dataset_digests([(int(ids[i]), int(src[i]), b"", data[i].tobytes()) for i in range(n)], declared=declared)
+    for rank in range(world):
+        got = results[rank]
+        for alg in ("sha256", "blake2b", "sha3-256"):
+            assert got[alg] == porc.inplace_merkle(alg, tensors, 8192).hex(), (rank, alg)
+        assert got["lattice"] == {k: (v[0].hex(), v[1]) for k, v in want_lat.items()}, rank
