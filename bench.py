@@ -315,6 +315,9 @@ def run_ours(args):
                                      f"{SHA256_ALU_INSTR_PER_LEAF:,} of them on the ALU pipe and the additions as "
                                      "IMAD on the FMA pipe, so achieved_tops may exceed the ALU-only peak",
                         "microbench": peaks}
+            # the unit that actually binds this kernel, next to the contractual HBM fraction
+            roofline["binding_unit"] = "integer ALU pipe (SHF/LOP3/PRMT at 64 lanes/clk/SM)"
+            roofline["binding_unit_frac"] = int_pipe["alu_pipe_utilisation"]
         except Exception as exc:       # the microbenchmark is evidence, not a dependency
             int_pipe = {"error": str(exc)}
 
