@@ -1,7 +1,7 @@
 """State-dict layouts of the benchmark architectures, without instantiating them.
 
 The benchmark configs (BASELINE.json) hash random-init fp32 weights of GPT-2,
-GPT2-XL, BERT-large and VGG19. Only the ordered list of (name, shape) matters to
+GPT2-XL, BERT-large and VGG19; bert-base and ResNet152 complete the paper's model table. Only the ordered list of (name, shape) matters to
 the hashing path, so the layouts are derived here from the architecture
 hyper-parameters; they reproduce the ``state_dict()`` entry order and sizes of
 ``transformers`` 5.5 / ``torchvision`` 0.26 (149 / 581 / 391 /
@@ -76,11 +76,43 @@ def vgg19() -> Layout:
     return out
 
 
+def resnet_bottleneck(blocks=(3, 8, 36, 3), num_classes: int = 1000) -> Layout:
+    """torchvision ``resnet152`` (blocks 3-8-36-3): 932 state-dict entries, 241,378,168 bytes.
+
+    Every BatchNorm contributes weight, bias, running_mean, running_var and the int64 scalar
+    ``num_batches_tracked`` (8 bytes -- listed here as two fp32 words, same byte count): the
+    many-tiny-tensors end of the paper's model table.
+    """
+    out: Layout = []
+
+    def bn(prefix: str, c: int) -> None:
+        out.extend([(prefix + ".weight", (c,), None), (prefix + ".bias", (c,), None),
+                    (prefix + ".running_mean", (c,), None), (prefix + ".running_var", (c,), None),
+                    (prefix + ".num_batches_tracked", (2,), None)])
+
+    out.append(("conv1.weight", (64, 3, 7, 7), None))
+    bn("bn1", 64)
+    cin = 64
+    for stage, (n_blocks, width) in enumerate(zip(blocks, (64, 128, 256, 512)), start=1):
+        for b in range(n_blocks):
+            p = f"layer{stage}.{b}."
+            out.append((p + "conv1.weight", (width, cin, 1, 1), None)); bn(p + "bn1", width)
+            out.append((p + "conv2.weight", (width, width, 3, 3), None)); bn(p + "bn2", width)
+            out.append((p + "conv3.weight", (4 * width, width, 1, 1), None)); bn(p + "bn3", 4 * width)
+            if b == 0:
+                out.append((p + "downsample.0.weight", (4 * width, cin, 1, 1), None)); bn(p + "downsample.1", 4 * width)
+            cin = 4 * width
+    out += [("fc.weight", (num_classes, cin), None), ("fc.bias", (num_classes,), None)]
+    return out
+
+
 ARCHITECTURES = {
     "gpt2": lambda: gpt2_lm_head(768, 12),
     "gpt2-xl": lambda: gpt2_lm_head(1600, 48),
     "bert-large": lambda: bert_model(1024, 24, 4096),
     "vgg19": vgg19,
+    "bert-base": lambda: bert_model(768, 12, 3072),
+    "resnet152": resnet_bottleneck,
 }
 
 

@@ -157,10 +157,23 @@ def test_dataset_manifest_round_trip_and_validation(tmp_path):
     ("gpt2-xl", 581, 6_552_089_600, 799_954, 388),
     ("bert-large", 391, 1_340_567_552, 163_753, 219),
     ("vgg19", 38, 574_668_960, 70_164, 18),
+    ("bert-base", 199, 437_928_960, 53_534, 125),          # SURVEY.md section 8, context rows
+    ("resnet152", 932, 241_378_168, 30_093, 761),
 ])
 def test_state_dict_layouts(arch, entries, nbytes, leaves, ragged):
     st = shapes.layout_stats(shapes.ARCHITECTURES[arch]())
     assert (st["entries"], st["bytes"], st["leaves"], st["ragged"]) == (entries, nbytes, leaves, ragged)
+
+
+def test_resnet152_layout_equals_torchvision():
+    tv = pytest.importorskip("torchvision")
+    import torch
+
+    with torch.device("meta"):
+        sd = tv.models.resnet152(weights=None).state_dict()
+    layout = shapes.ARCHITECTURES["resnet152"]()
+    assert [n for n, _, _ in layout] == list(sd.keys())
+    assert [shapes.numel(s) * 4 for _, s, _ in layout] == [v.numel() * v.element_size() for v in sd.values()]
 
 
 def test_gpt2_lm_head_is_tied():
