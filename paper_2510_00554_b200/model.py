@@ -20,6 +20,8 @@ from dataclasses import dataclass
 from pathlib import Path
 from typing import Dict, List, Optional, Tuple, Union
 
+import threading
+
 import numpy as np
 import torch
 
@@ -217,44 +219,151 @@ def _host_tensor(buf) -> torch.Tensor:
         return torch.from_numpy(arr)
 
 
-def _inplace_merkle_staged(cfg: HashConfig, model: TensorMap) -> ModelDigestResult:
+STAGE_RING_SLOTS = 4
+STAGE_SLOT_BYTES = 32 << 20            # one pinned staging buffer = one H2D transfer
+STAGE_PIECE_BYTES = 4 << 20            # memcpy granularity handed to the staging threads
+_ARENA_ALIGN = 256
+
+
+class _StagingRing:
+    """Pinned bounce buffers + memcpy threads for host memory that is not page-locked.
+
+    ``bytes`` / numpy / ordinary CPU tensors cannot be the source of an asynchronous DMA: a plain
+    ``cudaMemcpy`` from them runs at ~10 GB/s through the driver's own small bounce buffer. Here a few
+    threads copy the pageable bytes into a ring of pinned 32 MB buffers (numpy releases the GIL for
+    the memcpy) and every full buffer goes to the device as ONE asynchronous transfer while the next
+    buffer is being filled. The ring is created once per process.
+    """
+
+    _instance: Optional["_StagingRing"] = None
+
+    def __init__(self, threads: int):
+        from concurrent.futures import ThreadPoolExecutor
+
+        self.bufs = [torch.empty(STAGE_SLOT_BYTES, dtype=torch.uint8, pin_memory=True) for _ in range(STAGE_RING_SLOTS)]
+        self.views = [b.numpy() for b in self.bufs]
+        self.events: List[Optional[torch.cuda.Event]] = [None] * STAGE_RING_SLOTS
+        self.threads = threads
+        self.lock = threading.Lock()         # one staged hash at a time owns the ring (hash_model stays thread-safe)
+        self.pool = ThreadPoolExecutor(max_workers=threads, thread_name_prefix="snt-stage")
+        self.slot = 0
+
+    @classmethod
+    def get(cls, threads: int) -> "_StagingRing":
+        if cls._instance is None or cls._instance.threads < threads or \
+                cls._instance.bufs[0].numel() != STAGE_SLOT_BYTES:
+            cls._instance = cls(threads)
+        return cls._instance
+
+    def acquire(self) -> int:
+        """Next slot, once the transfer that last used it has completed."""
+        slot = self.slot
+        self.slot = (slot + 1) % STAGE_RING_SLOTS
+        if self.events[slot] is not None:
+            self.events[slot].synchronize()
+        return slot
+
+
+def _staging_threads(workers: int) -> int:
+    import os
+
+    return max(1, min(16, max(int(workers), min(8, os.cpu_count() or 1))))
+
+
+def _inplace_merkle_staged(cfg: HashConfig, model: TensorMap, workers: int = 1) -> ModelDigestResult:
     """Host tensors -> device with the copies and the leaf hashing overlapped.
 
-    Device buffers are allocated up front (the plan needs their addresses); the
-    copies run on a side stream in ~256 MB groups of whole tensors and the leaf
-    kernel for a group is enqueued as soon as its bytes have landed. The tree
-    reduction runs once at the end over the leaf digests.
+    Device buffers are allocated up front (the plan needs their addresses): tensors that are already
+    on the GPU stay where they are, pinned host tensors get their own device buffer and are copied
+    directly, and pageable host buffers are laid out back to back (256-byte aligned) in one device
+    arena and travel through the pinned staging ring in 32 MB transfers. All copies run on a side
+    stream; the leaf kernel for a ~256 MB group of whole tensors is enqueued as soon as its bytes
+    have landed, and the tree reduction runs once at the end over the leaf digests.
     """
     dev = _dev.require_cuda()
     bs = cfg.block_size
-    sizes = [buffer_nbytes(buf) for _, buf in model.entries]
+    entries = model.entries
+    sizes = [buffer_nbytes(buf) for _, buf in entries]
+    CUDA, PINNED, PAGEABLE = 0, 1, 2
+    kinds, arena_off, arena_total = [], [0] * len(entries), 0
+    for i, (_, buf) in enumerate(entries):
+        if _is_cuda(buf):
+            kinds.append(CUDA)
+        elif isinstance(buf, torch.Tensor) and buf.is_pinned():
+            kinds.append(PINNED)
+        else:
+            kinds.append(PAGEABLE)
+            arena_off[i] = arena_total
+            arena_total += -(-sizes[i] // _ARENA_ALIGN) * _ARENA_ALIGN
+    arena = torch.empty(max(arena_total, 16), dtype=torch.uint8, device=dev)
     dst: List[torch.Tensor] = []
-    for (_, buf), nbytes in zip(model.entries, sizes):
-        dst.append(_dev.as_device_bytes(buf, dev) if _is_cuda(buf) else
-                   torch.empty(nbytes, dtype=torch.uint8, device=dev))
+    for i, (_, buf) in enumerate(entries):
+        if kinds[i] == CUDA:
+            dst.append(_dev.as_device_bytes(buf, dev))
+        elif kinds[i] == PINNED:
+            dst.append(torch.empty(sizes[i], dtype=torch.uint8, device=dev))
+        else:
+            dst.append(arena[arena_off[i]:arena_off[i] + sizes[i]])
     plan = _dev.ModelPlan(dst, bs)
     try:
         hasher = _dev.MerkleModelHasher(plan, cfg.alg.value)
         main = torch.cuda.current_stream()
         side = torch.cuda.Stream()
         side.wait_stream(main)
-        first, group_begin, group_bytes, pending = 0, 0, 0, []
+        ring = _StagingRing.get(_staging_threads(workers)) if arena_total else None
+        if ring is not None:
+            ring.lock.acquire()
+        # the staging buffer being filled mirrors the arena range [chunk_base, chunk_base + chunk_fill)
+        slot, chunk_base, chunk_fill, tasks = -1, 0, 0, []
+
+        def flush_chunk():
+            nonlocal slot, chunk_fill, tasks
+            if slot < 0 or chunk_fill == 0:
+                return
+            for t in tasks:
+                t.result()
+            with torch.cuda.stream(side):
+                arena[chunk_base:chunk_base + chunk_fill].copy_(ring.bufs[slot][:chunk_fill], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(side)
+            ring.events[slot] = ev
+            slot, chunk_fill, tasks = -1, 0, []
+
+        first, group_begin, group_bytes = 0, 0, 0
         n = len(dst)
-        for i, (_, buf) in enumerate(model.entries):
-            if not _is_cuda(buf) and sizes[i]:
-                pending.append(i)
+        for i, (_, buf) in enumerate(entries):
+            if kinds[i] == PINNED and sizes[i]:
+                with torch.cuda.stream(side):
+                    dst[i].copy_(_host_tensor(buf), non_blocking=True)
+            elif kinds[i] == PAGEABLE and sizes[i]:
+                src = _host_tensor(buf).numpy() if isinstance(buf, torch.Tensor) else _dev.host_bytes_view(buf)
+                pos = 0
+                while pos < sizes[i]:
+                    if slot < 0:
+                        slot, chunk_base = ring.acquire(), arena_off[i] + pos
+                    so = arena_off[i] + pos - chunk_base
+                    if so >= STAGE_SLOT_BYTES:
+                        flush_chunk()
+                        continue
+                    take = min(sizes[i] - pos, STAGE_SLOT_BYTES - so)
+                    view = ring.views[slot]
+                    for p0 in range(0, take, STAGE_PIECE_BYTES):
+                        p1 = min(take, p0 + STAGE_PIECE_BYTES)
+                        tasks.append(ring.pool.submit(np.copyto, view[so + p0:so + p1], src[pos + p0:pos + p1]))
+                    chunk_fill = so + take
+                    pos += take
+                    if chunk_fill >= STAGE_SLOT_BYTES:
+                        flush_chunk()
             group_bytes += sizes[i]
             first_next = first + -(-sizes[i] // bs)
             if group_bytes >= STAGE_CHUNK_BYTES or i == n - 1:
-                with torch.cuda.stream(side):
-                    for j in pending:
-                        dst[j].copy_(_host_tensor(model.entries[j][1]), non_blocking=True)
-                    done = torch.cuda.Event()
-                    done.record(side)
+                flush_chunk()
+                done = torch.cuda.Event()
+                done.record(side)
                 main.wait_event(done)
                 if first_next > group_begin:
                     hasher.run_leaves_only(group_begin, first_next)
-                group_begin, group_bytes, pending = first_next, 0, []
+                group_begin, group_bytes = first_next, 0
             first = first_next
         hasher.run_tree_only()
         root = Digest(cfg.alg, hasher.out_bytes())          # synchronises: all copies and kernels done
@@ -262,6 +371,9 @@ def _inplace_merkle_staged(cfg: HashConfig, model: TensorMap) -> ModelDigestResu
         aux = hasher.leaves.numel() + hasher.work_bytes + (hasher.out.numel() if n_leaves > 1 else 0)
         return ModelDigestResult(root, cfg, n_leaves, aux_digest_bytes=aux)
     finally:
+        if 'ring' in locals() and ring is not None and ring.lock.locked():
+            torch.cuda.synchronize()          # no transfer may still read a staging buffer when the next owner starts
+            ring.lock.release()
         plan.close()
 
 
@@ -273,7 +385,7 @@ def inplace_hash(cfg: HashConfig, model: TensorMap, workers: int = 1) -> ModelDi
         _require_nonempty(model)
         host_bytes = sum(buffer_nbytes(buf) for buf in buffers if not _is_cuda(buf))
         if cfg.construction is Construction.MERKLE and host_bytes >= STAGE_PIPELINE_MIN_BYTES:
-            return _inplace_merkle_staged(cfg, model)
+            return _inplace_merkle_staged(cfg, model, workers)
     # an empty model is rejected by snt_model_plan_create (InvalidInput, model.py:166-168)
     plan = _dev.ModelPlan.from_spans(*_dev.device_spans(buffers), cfg.block_size)
     try:

@@ -228,6 +228,36 @@ def test_host_model_staged_in_overlapped_chunks(pkg, corc, monkeypatch):
         assert res.block_count == tl.leaf_count(8192)
 
 
+@pytest.mark.parametrize("slot_kb,piece_kb", [(1024, 256), (768, 1000), (32768, 4096)])
+def test_pageable_inputs_through_the_staging_ring(pkg, corc, monkeypatch, slot_kb, piece_kb):
+    """bytes / numpy / unpinned tensors ride the pinned ring: tensors straddle transfers, slots wrap around."""
+    from paper_2510_00554_b200 import model as mm
+
+    monkeypatch.setattr(mm, "STAGE_SLOT_BYTES", slot_kb << 10)
+    monkeypatch.setattr(mm, "STAGE_PIECE_BYTES", piece_kb << 10)
+    monkeypatch.setattr(mm, "STAGE_CHUNK_BYTES", 5 << 20)
+    rng = np.random.default_rng(12)
+    sizes = [(3 << 20) + 77, 1, 0, 8192 * 300, (6 << 20) + 8191, 255, 257, (11 << 20) + 5, 4096, (9 << 20)]
+    host = [rng.integers(0, 256, size=s, dtype=np.uint8) for s in sizes]
+    entries = []
+    for i, h in enumerate(host):
+        kind = i % 4
+        buf = h.tobytes() if kind == 0 else h if kind == 1 else torch.from_numpy(h.copy()) if kind == 2 \
+            else torch.from_numpy(h).view(torch.uint8)
+        if i == 4:
+            buf = torch.from_numpy(h[:-3].copy()).view(torch.float32)      # a float tensor, pageable
+            host[i] = h[:-3]
+        if i == 7:
+            buf = torch.from_numpy(h).pin_memory()                         # one pinned entry in between
+        entries.append((f"t{i}", buf))
+    tl = corc.TensorList(host)
+    for name in ALGS:
+        cfg = pkg.HashConfig(pkg.Construction.MERKLE, pkg.Strategy.IN_PLACE, _alg(pkg, name), 8192)
+        for workers in (1, 3):
+            res = pkg.hash_model(cfg, pkg.TensorMap(entries), workers=workers)
+            assert res.model_digest.data == corc.inplace_merkle(name, tl, 8192, 4), (name, workers)
+
+
 def test_per_layer_full_size_vgg19_against_oracle(pkg, porc):
     """38 layer digests of the VGG19 layout (scaled) for both constructions, against the oracle."""
     sd = _synthetic("vgg19", scale=0.06)
