@@ -9,6 +9,7 @@ functions -- without a CUDA device they raise ``ResourceError``.
 from __future__ import annotations
 
 import ctypes
+import threading
 import warnings
 from typing import Iterable, List, Optional, Sequence, Tuple
 
@@ -60,15 +61,102 @@ def as_device_bytes(buf, device: Optional[torch.device] = None) -> torch.Tensor:
         if t.dtype != torch.uint8:
             t = t.view(torch.uint8)
         if t.device.type != "cuda":
+            if t.numel() >= STAGE_DIRECT_MAX_BYTES and not t.is_pinned():
+                out = torch.empty(t.numel(), dtype=torch.uint8, device=device)
+                pageable_to_device(t.numpy(), out)
+                return out
             t = t.to(device, non_blocking=True)
         return t
     arr = host_bytes_view(buf)
     if arr.size == 0:
         return torch.empty(0, dtype=torch.uint8, device=device)
+    if arr.size >= STAGE_DIRECT_MAX_BYTES:
+        out = torch.empty(arr.size, dtype=torch.uint8, device=device)
+        pageable_to_device(arr, out)
+        return out
     with warnings.catch_warnings():
         warnings.simplefilter("ignore")          # read-only buffers are only read
         host = torch.from_numpy(arr)
     return host.to(device, non_blocking=True)
+
+
+STAGE_RING_SLOTS = 4
+STAGE_SLOT_BYTES = 32 << 20            # one pinned staging buffer = one H2D transfer
+STAGE_PIECE_BYTES = 4 << 20            # memcpy granularity handed to the staging threads
+
+
+class StagingRing:
+    """Pinned bounce buffers + memcpy threads for host memory that is not page-locked.
+
+    ``bytes`` / numpy / ordinary CPU tensors cannot be the source of an asynchronous DMA: a plain
+    ``cudaMemcpy`` from them runs at ~10 GB/s through the driver's own small bounce buffer. Here a few
+    threads copy the pageable bytes into a ring of pinned 32 MB buffers (numpy releases the GIL for
+    the memcpy) and every full buffer goes to the device as ONE asynchronous transfer while the next
+    buffer is being filled. The ring is created once per process.
+    """
+
+    _instance: Optional["StagingRing"] = None
+
+    def __init__(self, threads: int):
+        from concurrent.futures import ThreadPoolExecutor
+
+        self.bufs = [torch.empty(STAGE_SLOT_BYTES, dtype=torch.uint8, pin_memory=True) for _ in range(STAGE_RING_SLOTS)]
+        self.views = [b.numpy() for b in self.bufs]
+        self.events: List[Optional[torch.cuda.Event]] = [None] * STAGE_RING_SLOTS
+        self.threads = threads
+        self.lock = threading.Lock()         # one staged hash at a time owns the ring (hash_model stays thread-safe)
+        self.pool = ThreadPoolExecutor(max_workers=threads, thread_name_prefix="snt-stage")
+        self.slot = 0
+
+    @classmethod
+    def get(cls, threads: int) -> "StagingRing":
+        if cls._instance is None or cls._instance.threads < threads or \
+                cls._instance.bufs[0].numel() != STAGE_SLOT_BYTES:
+            cls._instance = cls(threads)
+        return cls._instance
+
+    def acquire(self) -> int:
+        """Next slot, once the transfer that last used it has completed."""
+        slot = self.slot
+        self.slot = (slot + 1) % STAGE_RING_SLOTS
+        if self.events[slot] is not None:
+            self.events[slot].synchronize()
+        return slot
+
+
+def staging_threads(workers: int = 1) -> int:
+    import os
+
+    return max(1, min(16, max(int(workers), min(8, os.cpu_count() or 1))))
+
+
+STAGE_DIRECT_MAX_BYTES = 8 << 20       # smaller pageable buffers take the plain (synchronous) copy
+
+
+def pageable_to_device(src: np.ndarray, dst: torch.Tensor, workers: int = 1) -> None:
+    """Copy a flat uint8 host array into ``dst`` (flat uint8 CUDA tensor) through the pinned ring.
+
+    Enqueues the transfers on the current stream and returns when the last memcpy into a staging
+    buffer is done; the device copy itself completes in stream order.
+    """
+    ring = StagingRing.get(staging_threads(workers))
+    stream = torch.cuda.current_stream()
+    n = int(src.shape[0])
+    with ring.lock:
+        for base in range(0, n, STAGE_SLOT_BYTES):
+            take = min(STAGE_SLOT_BYTES, n - base)
+            slot = ring.acquire()
+            view = ring.views[slot]
+            tasks = [ring.pool.submit(np.copyto, view[p0:min(take, p0 + STAGE_PIECE_BYTES)],
+                                      src[base + p0:base + min(take, p0 + STAGE_PIECE_BYTES)])
+                     for p0 in range(0, take, STAGE_PIECE_BYTES)]
+            for t in tasks:
+                t.result()
+            dst[base:base + take].copy_(ring.bufs[slot][:take], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(stream)
+            ring.events[slot] = ev
+        stream.synchronize()      # the ring may be handed to another caller / stream after the lock is released
 
 
 def device_spans(buffers: Sequence[object], device: Optional[torch.device] = None):

@@ -219,55 +219,7 @@ def _host_tensor(buf) -> torch.Tensor:
         return torch.from_numpy(arr)
 
 
-STAGE_RING_SLOTS = 4
-STAGE_SLOT_BYTES = 32 << 20            # one pinned staging buffer = one H2D transfer
-STAGE_PIECE_BYTES = 4 << 20            # memcpy granularity handed to the staging threads
 _ARENA_ALIGN = 256
-
-
-class _StagingRing:
-    """Pinned bounce buffers + memcpy threads for host memory that is not page-locked.
-
-    ``bytes`` / numpy / ordinary CPU tensors cannot be the source of an asynchronous DMA: a plain
-    ``cudaMemcpy`` from them runs at ~10 GB/s through the driver's own small bounce buffer. Here a few
-    threads copy the pageable bytes into a ring of pinned 32 MB buffers (numpy releases the GIL for
-    the memcpy) and every full buffer goes to the device as ONE asynchronous transfer while the next
-    buffer is being filled. The ring is created once per process.
-    """
-
-    _instance: Optional["_StagingRing"] = None
-
-    def __init__(self, threads: int):
-        from concurrent.futures import ThreadPoolExecutor
-
-        self.bufs = [torch.empty(STAGE_SLOT_BYTES, dtype=torch.uint8, pin_memory=True) for _ in range(STAGE_RING_SLOTS)]
-        self.views = [b.numpy() for b in self.bufs]
-        self.events: List[Optional[torch.cuda.Event]] = [None] * STAGE_RING_SLOTS
-        self.threads = threads
-        self.lock = threading.Lock()         # one staged hash at a time owns the ring (hash_model stays thread-safe)
-        self.pool = ThreadPoolExecutor(max_workers=threads, thread_name_prefix="snt-stage")
-        self.slot = 0
-
-    @classmethod
-    def get(cls, threads: int) -> "_StagingRing":
-        if cls._instance is None or cls._instance.threads < threads or \
-                cls._instance.bufs[0].numel() != STAGE_SLOT_BYTES:
-            cls._instance = cls(threads)
-        return cls._instance
-
-    def acquire(self) -> int:
-        """Next slot, once the transfer that last used it has completed."""
-        slot = self.slot
-        self.slot = (slot + 1) % STAGE_RING_SLOTS
-        if self.events[slot] is not None:
-            self.events[slot].synchronize()
-        return slot
-
-
-def _staging_threads(workers: int) -> int:
-    import os
-
-    return max(1, min(16, max(int(workers), min(8, os.cpu_count() or 1))))
 
 
 def _inplace_merkle_staged(cfg: HashConfig, model: TensorMap, workers: int = 1) -> ModelDigestResult:
@@ -310,7 +262,7 @@ def _inplace_merkle_staged(cfg: HashConfig, model: TensorMap, workers: int = 1) 
         main = torch.cuda.current_stream()
         side = torch.cuda.Stream()
         side.wait_stream(main)
-        ring = _StagingRing.get(_staging_threads(workers)) if arena_total else None
+        ring = _dev.StagingRing.get(_dev.staging_threads(workers)) if arena_total else None
         if ring is not None:
             ring.lock.acquire()
         # the staging buffer being filled mirrors the arena range [chunk_base, chunk_base + chunk_fill)
@@ -342,17 +294,17 @@ def _inplace_merkle_staged(cfg: HashConfig, model: TensorMap, workers: int = 1) 
                     if slot < 0:
                         slot, chunk_base = ring.acquire(), arena_off[i] + pos
                     so = arena_off[i] + pos - chunk_base
-                    if so >= STAGE_SLOT_BYTES:
+                    if so >= _dev.STAGE_SLOT_BYTES:
                         flush_chunk()
                         continue
-                    take = min(sizes[i] - pos, STAGE_SLOT_BYTES - so)
+                    take = min(sizes[i] - pos, _dev.STAGE_SLOT_BYTES - so)
                     view = ring.views[slot]
-                    for p0 in range(0, take, STAGE_PIECE_BYTES):
-                        p1 = min(take, p0 + STAGE_PIECE_BYTES)
+                    for p0 in range(0, take, _dev.STAGE_PIECE_BYTES):
+                        p1 = min(take, p0 + _dev.STAGE_PIECE_BYTES)
                         tasks.append(ring.pool.submit(np.copyto, view[so + p0:so + p1], src[pos + p0:pos + p1]))
                     chunk_fill = so + take
                     pos += take
-                    if chunk_fill >= STAGE_SLOT_BYTES:
+                    if chunk_fill >= _dev.STAGE_SLOT_BYTES:
                         flush_chunk()
             group_bytes += sizes[i]
             first_next = first + -(-sizes[i] // bs)

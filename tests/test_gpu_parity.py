@@ -231,10 +231,10 @@ def test_host_model_staged_in_overlapped_chunks(pkg, corc, monkeypatch):
 @pytest.mark.parametrize("slot_kb,piece_kb", [(1024, 256), (768, 1000), (32768, 4096)])
 def test_pageable_inputs_through_the_staging_ring(pkg, corc, monkeypatch, slot_kb, piece_kb):
     """bytes / numpy / unpinned tensors ride the pinned ring: tensors straddle transfers, slots wrap around."""
-    from paper_2510_00554_b200 import model as mm
+    from paper_2510_00554_b200 import device as dv, model as mm
 
-    monkeypatch.setattr(mm, "STAGE_SLOT_BYTES", slot_kb << 10)
-    monkeypatch.setattr(mm, "STAGE_PIECE_BYTES", piece_kb << 10)
+    monkeypatch.setattr(dv, "STAGE_SLOT_BYTES", slot_kb << 10)
+    monkeypatch.setattr(dv, "STAGE_PIECE_BYTES", piece_kb << 10)
     monkeypatch.setattr(mm, "STAGE_CHUNK_BYTES", 5 << 20)
     rng = np.random.default_rng(12)
     sizes = [(3 << 20) + 77, 1, 0, 8192 * 300, (6 << 20) + 8191, 255, 257, (11 << 20) + 5, 4096, (9 << 20)]
@@ -256,6 +256,11 @@ def test_pageable_inputs_through_the_staging_ring(pkg, corc, monkeypatch, slot_k
         for workers in (1, 3):
             res = pkg.hash_model(cfg, pkg.TensorMap(entries), workers=workers)
             assert res.model_digest.data == corc.inplace_merkle(name, tl, 8192, 4), (name, workers)
+    # the generic helper behind as_device_bytes (dataset shards, lattice / per-layer / coalesced model paths)
+    monkeypatch.setattr(dv, "STAGE_DIRECT_MAX_BYTES", 1 << 20)
+    big = rng.integers(0, 256, size=(7 << 20) + 321, dtype=np.uint8)
+    for src in (big.tobytes(), big, torch.from_numpy(big.copy())):
+        assert bytes(dv.as_device_bytes(src).cpu().numpy().tobytes()) == big.tobytes()
 
 
 def test_per_layer_full_size_vgg19_against_oracle(pkg, porc):
