@@ -155,6 +155,20 @@ int snt_merkle_roots_segmented(int alg, const void* d_digests, const uint64_t* s
                                uint32_t n_segments, const void* d_empty_digest, void* d_work,
                                size_t work_bytes, void* d_out, snt_stream_t stream);
 
+/* Data movement of the strategies that copy before hashing: span i =
+ * d_len[i] bytes at device address d_src_addr[i] goes to d_dst + d_dst_off[i];
+ * with pad_block != 0 the span is zero-filled up to the next multiple of
+ * pad_block. coalesce_hash (model.py:203-228) packs every tensor this way
+ * (pad_block = 0); per_layer_hash (model.py:245-253) zero-pads the ragged last
+ * block of each tensor (pad_block = block size, spans = the tails only).
+ * d_chunk_first[n_spans + 1] is the running count of 32 KiB chunks
+ * (snt_gather_chunk_bytes) of the padded spans; n_chunks = its last entry.
+ * All four arrays are DEVICE pointers. Destination ranges must not overlap. */
+uint32_t snt_gather_chunk_bytes(void);
+int snt_gather_spans(const uint64_t* d_src_addr, const uint64_t* d_len, const uint64_t* d_dst_off,
+                     const uint64_t* d_chunk_first, uint32_t n_spans, uint64_t n_chunks,
+                     uint32_t pad_block, void* d_dst, snt_stream_t stream);
+
 /* lt_reduce (lattice.py:104-119): add n 64-byte digests into d_acc[32]. */
 int snt_lt_reduce(const void* d_digests, uint64_t n, uint32_t* d_acc, snt_stream_t stream);
 

@@ -35,6 +35,9 @@ SIGNATURES = {
     "snt_model_plan_leaf_count": (c_uint64, [c_void_p]),
     "snt_model_plan_total_bytes": (c_uint64, [c_void_p]),
     "snt_merkle_work_bytes": (c_size_t, [c_int, c_uint64]),
+    "snt_gather_chunk_bytes": (c_uint32, []),
+    "snt_gather_spans": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_uint32, c_uint64, c_uint32, c_void_p,
+                                 c_void_p]),
     "snt_merkle_leaves": (c_int, [c_void_p, c_int, c_uint64, c_uint64, c_void_p, c_void_p]),
     "snt_merkle_inplace": (c_int, [c_void_p, c_int, c_uint64, c_uint64, c_uint32, c_void_p, c_void_p,
                                    c_size_t, c_void_p, c_void_p]),

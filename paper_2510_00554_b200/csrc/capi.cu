@@ -10,6 +10,7 @@
 #include <vector>
 
 #include "../../include/sentinel_b200.h"
+#include "gather_kernels.cuh"
 #include "lthash_kernels.cuh"
 #include "merkle_kernels.cuh"
 
@@ -445,19 +446,72 @@ int snt_merkle_roots_segmented(int alg, const void* d_digests, const uint64_t* s
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const uint8_t* in = static_cast<const uint8_t*>(d_digests);
     uint8_t* out = static_cast<uint8_t*>(d_out);
+    // segments that fit one CTA (<= 2^max_levels digests) share ONE launch; the rest go one by one
+    const uint64_t cta_cap = 1ull << max_levels(alg);
+    std::vector<uint64_t> table;           // [begin, count] per small segment, then the u32 output indices
+    std::vector<uint32_t> out_idx;
     for (uint32_t t = 0; t < n_segments; ++t) {
         if (seg_first[t + 1] < seg_first[t]) return SNT_ERR_INVALID_INPUT;
         const uint64_t count = seg_first[t + 1] - seg_first[t];
-        if (count == 0) {
-            if (!d_empty_digest) return SNT_ERR_INVALID_INPUT;
-            SNT_CUDA(cudaMemcpyAsync(out + static_cast<size_t>(t) * dlen, d_empty_digest, dlen,
-                                     cudaMemcpyDeviceToDevice, s));
-            continue;
+        if (count == 0 && !d_empty_digest) return SNT_ERR_INVALID_INPUT;
+        if (count <= cta_cap) {
+            table.push_back(seg_first[t]);
+            table.push_back(count);
+            out_idx.push_back(t);
         }
+    }
+    if (!out_idx.empty()) {
+        const size_t n_small = out_idx.size();
+        const size_t seg_bytes = table.size() * sizeof(uint64_t);
+        table.resize(table.size() + (n_small + 1) / 2);
+        memcpy(reinterpret_cast<uint8_t*>(table.data()) + seg_bytes, out_idx.data(), n_small * sizeof(uint32_t));
+        uint64_t* d_table = nullptr;
+        SNT_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_table), table.size() * sizeof(uint64_t), s));
+        // pageable source: the call returns once the bytes sit in the driver's staging buffer
+        cudaError_t e = cudaMemcpyAsync(d_table, table.data(), table.size() * sizeof(uint64_t), cudaMemcpyHostToDevice, s);
+        if (e == cudaSuccess) {
+            const uint32_t* d_idx = reinterpret_cast<const uint32_t*>(reinterpret_cast<const uint8_t*>(d_table) + seg_bytes);
+            const uint8_t* empty = static_cast<const uint8_t*>(d_empty_digest);
+            const MerkleConsts& c = node_consts();
+            const unsigned grid = static_cast<unsigned>(n_small);
+            switch (alg) {
+                case SNT_SHA256:
+                    merkle_reduce_segments_kernel<ALG_SHA256, 256><<<grid, 256, 0, s>>>(in, d_table, d_idx, empty, c, out);
+                    break;
+                case SNT_BLAKE2B:
+                    merkle_reduce_segments_kernel<ALG_BLAKE2B, 256><<<grid, 256, 0, s>>>(in, d_table, d_idx, empty, c, out);
+                    break;
+                default:
+                    merkle_reduce_segments_kernel<ALG_SHA3_256, 256><<<grid, 256, 0, s>>>(in, d_table, d_idx, empty, c, out);
+            }
+            e = cudaGetLastError();
+            ++g_launches;
+        }
+        cudaFreeAsync(d_table, s);
+        if (e != cudaSuccess) return cuda_fail(e, "snt_merkle_roots_segmented");
+    }
+    for (uint32_t t = 0; t < n_segments; ++t) {
+        const uint64_t count = seg_first[t + 1] - seg_first[t];
+        if (count <= cta_cap) continue;
         const int rc = snt_merkle_root(alg, in + seg_first[t] * dlen, count, d_work, work_bytes,
                                        out + static_cast<size_t>(t) * dlen, stream);
         if (rc != SNT_OK) return rc;
     }
+    return SNT_OK;
+}
+
+uint32_t snt_gather_chunk_bytes(void) { return GATHER_CHUNK_BYTES; }
+
+int snt_gather_spans(const uint64_t* d_src_addr, const uint64_t* d_len, const uint64_t* d_dst_off,
+                     const uint64_t* d_chunk_first, uint32_t n_spans, uint64_t n_chunks,
+                     uint32_t pad_block, void* d_dst, snt_stream_t stream) {
+    if (n_spans == 0 || n_chunks == 0) return SNT_OK;
+    if (!d_src_addr || !d_len || !d_dst_off || !d_chunk_first || !d_dst) return SNT_ERR_INVALID_INPUT;
+    if (n_chunks > 0x7fffffffull) return SNT_ERR_INVALID_INPUT;
+    gather_spans_kernel<<<static_cast<unsigned>(n_chunks), GATHER_THREADS, 0, static_cast<cudaStream_t>(stream)>>>(
+        d_src_addr, d_len, d_dst_off, d_chunk_first, n_spans, pad_block, static_cast<uint8_t*>(d_dst));
+    SNT_CUDA(cudaGetLastError());
+    ++g_launches;
     return SNT_OK;
 }
 

@@ -200,19 +200,16 @@ SNT_D void pair_or_pad(uint32_t* left, const uint32_t* right, bool right_exists,
     for (int i = 0; i < A::DW; ++i) left[i] = out[i];
 }
 
+// The reduction of one aligned group of 2^levels inputs starting at global node index `base` (see
+// above); writes the group's single output node to out_digest. Called by every thread of the CTA.
 template <int ALG, int THREADS>
-__global__ void __launch_bounds__(THREADS)
-merkle_reduce_kernel(const uint8_t* __restrict__ in, uint64_t first, uint64_t n_in,
-                     uint64_t level_count, uint32_t levels, const __grid_constant__ MerkleConsts c,
-                     uint8_t* __restrict__ out) {
+SNT_D void reduce_group(const uint8_t* __restrict__ in, uint64_t first, uint64_t n_in, uint64_t base,
+                        uint64_t level_count, uint32_t levels, const MerkleConsts& c,
+                        uint8_t* __restrict__ out_digest, uint32_t* buf_a, uint32_t* buf_b) {
     using A = AlgTraits<ALG>;
     constexpr int DW = A::DW;
     constexpr int CAP = ReduceShape<ALG>::CAP;
-    __shared__ uint32_t buf_a[DW * CAP];
-    __shared__ uint32_t buf_b[DW * CAP / 2];
-
     const uint32_t tid = threadIdx.x;
-    const uint64_t base = first + (static_cast<uint64_t>(blockIdx.x) << levels);   // first input of this CTA
     const uint64_t in_end = first + n_in;
     const uint32_t width = 1u << levels;
 
@@ -261,8 +258,48 @@ merkle_reduce_kernel(const uint8_t* __restrict__ in, uint64_t first, uint64_t n_
         uint32_t d[DW];
 #pragma unroll
         for (int i = 0; i < DW; ++i) d[i] = src[i * src_stride];
-        store_digest<ALG>(out + static_cast<uint64_t>(blockIdx.x) * A::DIGEST_BYTES, d);
+        store_digest<ALG>(out_digest, d);
     }
+}
+
+template <int ALG, int THREADS>
+__global__ void __launch_bounds__(THREADS)
+merkle_reduce_kernel(const uint8_t* __restrict__ in, uint64_t first, uint64_t n_in,
+                     uint64_t level_count, uint32_t levels, const __grid_constant__ MerkleConsts c,
+                     uint8_t* __restrict__ out) {
+    using A = AlgTraits<ALG>;
+    constexpr int CAP = ReduceShape<ALG>::CAP;
+    __shared__ uint32_t buf_a[A::DW * CAP];
+    __shared__ uint32_t buf_b[A::DW * CAP / 2];
+    const uint64_t base = first + (static_cast<uint64_t>(blockIdx.x) << levels);   // first input of this CTA
+    reduce_group<ALG, THREADS>(in, first, n_in, base, level_count, levels, c,
+                               out + static_cast<uint64_t>(blockIdx.x) * A::DIGEST_BYTES, buf_a, buf_b);
+}
+
+// One tree per segment (per_layer_hash, model.py:245-253), one CTA per segment, one launch for all
+// segments of at most 2^MAX_LEVELS digests: segment j covers digests [seg[2j], seg[2j] + seg[2j+1]) of
+// `in` and its root goes to out + seg_out[j] * DIGEST_BYTES. The root of a tree of `count` nodes under
+// the reference rule (merkle.py:152-165) is the result of exactly ceil(log2(count)) levels; a single
+// digest is its own root and an empty segment takes the digest of the empty message.
+template <int ALG, int THREADS>
+__global__ void __launch_bounds__(THREADS)
+merkle_reduce_segments_kernel(const uint8_t* __restrict__ in, const uint64_t* __restrict__ seg,
+                              const uint32_t* __restrict__ seg_out, const uint8_t* __restrict__ empty_digest,
+                              const __grid_constant__ MerkleConsts c, uint8_t* __restrict__ out) {
+    using A = AlgTraits<ALG>;
+    constexpr int CAP = ReduceShape<ALG>::CAP;
+    __shared__ uint32_t buf_a[A::DW * CAP];
+    __shared__ uint32_t buf_b[A::DW * CAP / 2];
+    const uint64_t begin = seg[2ull * blockIdx.x], count = seg[2ull * blockIdx.x + 1];
+    uint8_t* dst = out + static_cast<uint64_t>(seg_out[blockIdx.x]) * A::DIGEST_BYTES;
+    if (count <= 1) {
+        const uint8_t* src = count ? in + begin * A::DIGEST_BYTES : empty_digest;
+        for (uint32_t i = threadIdx.x; i < A::DIGEST_BYTES; i += THREADS) dst[i] = src[i];
+        return;
+    }
+    uint32_t levels = 0;
+    while ((1ull << levels) < count) ++levels;
+    reduce_group<ALG, THREADS>(in + begin * A::DIGEST_BYTES, 0, count, 0, count, levels, c, dst, buf_a, buf_b);
 }
 
 }  // namespace snt

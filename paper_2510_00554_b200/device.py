@@ -131,6 +131,7 @@ def staging_threads(workers: int = 1) -> int:
 
 
 STAGE_DIRECT_MAX_BYTES = 8 << 20       # smaller pageable buffers take the plain (synchronous) copy
+STAGE_INLINE_MAX_BYTES = 256 << 10     # pieces below this are copied by the calling thread, not the pool
 
 
 def pageable_to_device(src: np.ndarray, dst: torch.Tensor, workers: int = 1) -> None:
@@ -159,28 +160,144 @@ def pageable_to_device(src: np.ndarray, dst: torch.Tensor, workers: int = 1) -> 
         stream.synchronize()      # the ring may be handed to another caller / stream after the lock is released
 
 
-def device_spans(buffers: Sequence[object], device: Optional[torch.device] = None):
+ARENA_ALIGN = 256
+
+
+def _host_array(buf) -> np.ndarray:
+    """Flat uint8 numpy view of a host buffer (bytes-like, numpy array or CPU tensor); zero copy when contiguous."""
+    if isinstance(buf, torch.Tensor):
+        t = buf.detach()
+        t = t if t.is_contiguous() else t.contiguous()
+        t = t.reshape(-1)
+        return (t if t.dtype == torch.uint8 else t.view(torch.uint8)).numpy()
+    return host_bytes_view(buf)
+
+
+def pageable_arena(arrays: Sequence[np.ndarray], device: torch.device, workers: int = 1):
+    """Lay host arrays back to back (256-byte aligned) in ONE device buffer, filled through the pinned ring.
+
+    Returns (arena tensor, byte offset of every array). Transfers are enqueued on the current stream.
+    """
+    offs, total = [], 0
+    for a in arrays:
+        offs.append(total)
+        total += -(-int(a.shape[0]) // ARENA_ALIGN) * ARENA_ALIGN
+    arena = torch.empty(max(total, 16), dtype=torch.uint8, device=device)
+    ring = StagingRing.get(staging_threads(workers))
+    stream = torch.cuda.current_stream()
+    with ring.lock:
+        slot, base, fill, tasks = -1, 0, 0, []
+
+        def flush():
+            nonlocal slot, fill, tasks
+            if slot < 0 or fill == 0:
+                return
+            for t in tasks:
+                t.result()
+            arena[base:base + fill].copy_(ring.bufs[slot][:fill], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(stream)
+            ring.events[slot] = ev
+            slot, fill, tasks = -1, 0, []
+
+        for a, off in zip(arrays, offs):
+            n, pos = int(a.shape[0]), 0
+            while pos < n:
+                if slot < 0:
+                    slot, base = ring.acquire(), off + pos
+                so = off + pos - base
+                if so >= STAGE_SLOT_BYTES:
+                    flush()
+                    continue
+                take = min(n - pos, STAGE_SLOT_BYTES - so)
+                view = ring.views[slot]
+                if take < STAGE_INLINE_MAX_BYTES:                 # a task costs more than a small memcpy
+                    np.copyto(view[so:so + take], a[pos:pos + take])
+                else:
+                    for p0 in range(0, take, STAGE_PIECE_BYTES):
+                        p1 = min(take, p0 + STAGE_PIECE_BYTES)
+                        tasks.append(ring.pool.submit(np.copyto, view[so + p0:so + p1], a[pos + p0:pos + p1]))
+                fill = so + take
+                pos += take
+                if fill >= STAGE_SLOT_BYTES:
+                    flush()
+        flush()
+        stream.synchronize()          # the ring goes back to the pool only when no transfer still reads it
+    return arena, offs
+
+
+def device_spans(buffers: Sequence[object], device: Optional[torch.device] = None, workers: int = 1):
     """(keep-alive list, addresses, byte lengths) of the buffers' bytes in HBM, in order.
 
     The fast path of the drop-in API: a contiguous CUDA tensor is described by its
     ``data_ptr()`` and ``nbytes`` alone -- no detach / reshape / view per tensor, which for a
     581-tensor state dict costs more host time than a GPT-2 small hash takes on the GPU.
-    Anything else (host memory, non-contiguous tensors) is staged through ``as_device_bytes``.
+    Host memory is staged: pinned tensors and small buffers by a direct copy each; when the
+    pageable buffers add up to more than a few MB they are packed into one device arena
+    through the pinned staging ring (``pageable_arena``) instead of one slow copy per buffer.
     """
     device = device or require_cuda()
     n = len(buffers)
     keep: List[object] = [None] * n
     ptrs = np.zeros(max(n, 1), dtype=np.uint64)
     sizes = np.zeros(max(n, 1), dtype=np.uint64)
+    pageable: List[int] = []
     for i, buf in enumerate(buffers):
-        if not (type(buf) is torch.Tensor and buf.is_cuda and buf.is_contiguous()):
+        if type(buf) is torch.Tensor and buf.is_cuda and buf.is_contiguous():
+            pass
+        elif isinstance(buf, torch.Tensor) and (buf.is_cuda or buf.is_pinned()):
             buf = as_device_bytes(buf, device)
+        else:
+            pageable.append(i)
+            continue
         nbytes = buf.nbytes
         keep[i] = buf
         sizes[i] = nbytes
         if nbytes:
             ptrs[i] = buf.data_ptr()
+    if pageable:
+        arrays = [_host_array(buffers[i]) for i in pageable]
+        if sum(int(a.shape[0]) for a in arrays) >= STAGE_DIRECT_MAX_BYTES:
+            arena, offs = pageable_arena(arrays, device, workers)
+            base = arena.data_ptr()
+            for i, a, off in zip(pageable, arrays, offs):
+                keep[i] = arena
+                sizes[i] = int(a.shape[0])
+                if sizes[i]:
+                    ptrs[i] = base + off
+        else:
+            for i in pageable:
+                t = as_device_bytes(buffers[i], device)
+                keep[i], sizes[i] = t, t.nbytes
+                if t.nbytes:
+                    ptrs[i] = t.data_ptr()
     return keep, ptrs, sizes
+
+
+def gather_spans(src_addr: np.ndarray, lengths: np.ndarray, dst_off: np.ndarray, pad_block: int,
+                 dst: torch.Tensor) -> None:
+    """``snt_gather_spans``: copy span i (``lengths[i]`` bytes at device address ``src_addr[i]``) to
+    ``dst[dst_off[i]:]``, zero-padded to a multiple of ``pad_block`` when that is non-zero. One launch."""
+    lib = _native.load()
+    n = int(lengths.shape[0])
+    if n == 0:
+        return
+    lengths = lengths.astype(np.uint64, copy=False)
+    padded = lengths if not pad_block else (lengths + np.uint64(pad_block - 1)) // np.uint64(pad_block) * np.uint64(pad_block)
+    chunk = int(lib.snt_gather_chunk_bytes())
+    chunk_first = np.zeros(n + 1, dtype=np.uint64)
+    np.cumsum((padded + np.uint64(chunk - 1)) // np.uint64(chunk), out=chunk_first[1:])
+    n_chunks = int(chunk_first[-1])
+    if n_chunks == 0:
+        return
+    table = np.concatenate([src_addr.astype(np.uint64, copy=False), lengths, dst_off.astype(np.uint64, copy=False),
+                            chunk_first])
+    d_table = torch.from_numpy(table.view(np.int64)).to(dst.device, non_blocking=False)
+    base = d_table.data_ptr()
+    rc = lib.snt_gather_spans(ctypes.c_void_p(base), ctypes.c_void_p(base + 8 * n), ctypes.c_void_p(base + 16 * n),
+                              ctypes.c_void_p(base + 24 * n), n, n_chunks, pad_block, _ptr(dst), _stream())
+    _native.check(rc, "snt_gather_spans")
+    d_table.record_stream(torch.cuda.current_stream())
 
 
 class ModelPlan:

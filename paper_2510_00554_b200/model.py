@@ -299,9 +299,12 @@ def _inplace_merkle_staged(cfg: HashConfig, model: TensorMap, workers: int = 1) 
                         continue
                     take = min(sizes[i] - pos, _dev.STAGE_SLOT_BYTES - so)
                     view = ring.views[slot]
-                    for p0 in range(0, take, _dev.STAGE_PIECE_BYTES):
-                        p1 = min(take, p0 + _dev.STAGE_PIECE_BYTES)
-                        tasks.append(ring.pool.submit(np.copyto, view[so + p0:so + p1], src[pos + p0:pos + p1]))
+                    if take < _dev.STAGE_INLINE_MAX_BYTES:            # a task costs more than a small memcpy
+                        np.copyto(view[so:so + take], src[pos:pos + take])
+                    else:
+                        for p0 in range(0, take, _dev.STAGE_PIECE_BYTES):
+                            p1 = min(take, p0 + _dev.STAGE_PIECE_BYTES)
+                            tasks.append(ring.pool.submit(np.copyto, view[so + p0:so + p1], src[pos + p0:pos + p1]))
                     chunk_fill = so + take
                     pos += take
                     if chunk_fill >= _dev.STAGE_SLOT_BYTES:
@@ -351,18 +354,22 @@ def coalesce_hash(cfg: HashConfig, model: TensorMap, workers: int = 1) -> ModelD
     _require_nonempty(model)
     dev = _dev.require_cuda()
     bs = cfg.block_size
-    total = model.total_bytes
+    keep, ptrs, sizes = _dev.device_spans([buf for _, buf in model.entries], dev)
+    n = len(keep)
+    total = int(sizes[:n].sum())
     padded = -(-total // bs) * bs
-    packed = torch.zeros(padded, dtype=torch.uint8, device=dev)
-    pos = 0
-    for t in device_tensors(model):
-        packed[pos:pos + t.numel()].copy_(t)
-        pos += t.numel()
+    packed = torch.empty(padded, dtype=torch.uint8, device=dev)
+    if padded > total:
+        packed[total:].zero_()
+    dst_off = np.zeros(n, dtype=np.uint64)
+    np.cumsum(sizes[:n - 1], out=dst_off[1:])
+    _dev.gather_spans(ptrs[:n], sizes[:n], dst_off, 0, packed)          # one launch for all tensors
     plan = _dev.ModelPlan([packed], bs)
     try:
         return _hash_plan(cfg, plan, aux_data_bytes=padded)
     finally:
         plan.close()
+        del keep
 
 
 def per_layer_hash(cfg: HashConfig, model: TensorMap, workers: int = 1) -> ModelDigestResult:
@@ -382,30 +389,34 @@ def per_layer_hash(cfg: HashConfig, model: TensorMap, workers: int = 1) -> Model
     dev = _dev.require_cuda()
     bs = cfg.block_size
     names = model.names()
-    flat = device_tensors(model)
-    sizes = [t.numel() for t in flat]
-    n_layers = len(flat)
-    block_counts = [-(-s // bs) for s in sizes]
+    keep, ptrs, sizes = _dev.device_spans([buf for _, buf in model.entries], dev)
+    n_layers = len(keep)
+    ptrs, sizes = ptrs[:n_layers], sizes[:n_layers]
+    block_counts = [int(c) for c in (sizes + np.uint64(bs - 1)) // np.uint64(bs)]
 
     if cfg.construction is Construction.MERKLE:
         alg = cfg.alg.value
         dlen = cfg.alg.digest_len
-        ragged = [i for i, s in enumerate(sizes) if s % bs]
-        scratch = torch.zeros(max(1, len(ragged)) * bs, dtype=torch.uint8, device=dev)
-        virt: List[torch.Tensor] = []
+        # span arithmetic only (no per-tensor device op): the full blocks of tensor i stay where they are,
+        # its ragged tail is gathered, zero-padded, into slot k of a scratch buffer (one launch for all tails)
+        full = sizes // np.uint64(bs) * np.uint64(bs)
+        tail = sizes - full
+        ragged = np.nonzero(tail)[0]
+        scratch = torch.empty(max(1, len(ragged)) * bs, dtype=torch.uint8, device=dev)
+        slot_addr = np.zeros(n_layers, dtype=np.uint64)
+        slot_addr[ragged] = np.uint64(scratch.data_ptr()) + np.arange(len(ragged), dtype=np.uint64) * np.uint64(bs)
+        if len(ragged):
+            _dev.gather_spans((ptrs + full)[ragged], tail[ragged], np.arange(len(ragged), dtype=np.uint64) * np.uint64(bs),
+                              bs, scratch)
+        v_ptrs = np.stack([ptrs, slot_addr], axis=1).reshape(-1)         # per tensor: (full part, padded tail)
+        v_sizes = np.stack([full, np.where(tail > 0, np.uint64(bs), np.uint64(0))], axis=1).reshape(-1)
+        live = np.nonzero(v_sizes)[0]
         seg_first = [0]
-        slot = 0
-        for i, t in enumerate(flat):
-            full = (sizes[i] // bs) * bs
-            if full:
-                virt.append(t[:full])
-            if sizes[i] % bs:
-                pad = scratch[slot * bs:(slot + 1) * bs]
-                pad[:sizes[i] - full].copy_(t[full:])
-                virt.append(pad)
-                slot += 1
-            seg_first.append(seg_first[-1] + block_counts[i])
-        plan = _dev.ModelPlan(virt, bs)
+        for c in block_counts:
+            seg_first.append(seg_first[-1] + c)
+        plan = _dev.ModelPlan.from_spans([None] * len(live), np.ascontiguousarray(v_ptrs[live]),
+                                         np.ascontiguousarray(v_sizes[live]), bs)
+        plan.tensors = [keep, scratch]                                   # the owners of the spans live as long as the plan
         try:
             hasher = _dev.MerkleModelHasher(plan, alg)
             hasher.run_leaves_only()
@@ -416,14 +427,14 @@ def per_layer_hash(cfg: HashConfig, model: TensorMap, workers: int = 1) -> Model
             layer_bytes = layers_dev.cpu().numpy().tobytes()
             root = Digest(cfg.alg, root_dev.cpu().numpy().tobytes())
             aux_digest = hasher.leaves.numel() + layers_dev.numel() + hasher.work_bytes
-            aux_data = scratch.numel() if ragged else 0
+            aux_data = scratch.numel() if len(ragged) else 0
         finally:
             plan.close()
         layer_digests = {name: Digest(cfg.alg, layer_bytes[i * dlen:(i + 1) * dlen]) for i, name in enumerate(names)}
         return ModelDigestResult(root, cfg, sum(block_counts), layer_digests=layer_digests,
                                  aux_data_bytes=aux_data, aux_digest_bytes=aux_digest)
 
-    plan = _dev.ModelPlan(flat, bs)
+    plan = _dev.ModelPlan.from_spans(keep, ptrs, sizes, bs)
     try:
         acc = _dev.LatticeAccumulator(n_layers)
         acc.add_model_layers(plan, 0, plan.leaf_count)

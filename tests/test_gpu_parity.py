@@ -667,3 +667,34 @@ def test_graph_replay_rehashes_current_bytes(pkg, porc):
     changed = [bytes(dts[0].cpu().numpy().tobytes())] + tensors[1:]
     graph.replay()                                          # ... and the same graph hashes the new bytes
     assert hasher.out_bytes() == porc.inplace_merkle("sha256", changed, 8192)
+
+
+def test_gather_spans_any_alignment(pkg):
+    """snt_gather_spans against numpy: every source/destination byte phase, zero padding, empty spans, >1 chunk."""
+    from paper_2510_00554_b200 import device as dev
+
+    rng = np.random.default_rng(99)
+    pool = torch.from_numpy(rng.integers(1, 256, size=6 << 20, dtype=np.uint8)).cuda()
+    host = pool.cpu().numpy()
+    for pad_block in (0, 64, 8192):
+        lens, src_off, dst_off, pos = [], [], [], 0
+        for k in range(200):
+            n = int(rng.choice([0, 1, 3, 15, 16, 17, 255, 4096, 8191, 8192, 40000, 70001, 300000][: 13 if k % 7 else 11]))
+            so = int(rng.integers(0, host.size - n - 1))
+            so = so - so % 16 + (k % 16)                       # every source phase
+            pos += (k * 5) % 16 if pad_block == 0 else 0       # every destination phase (packed layout only)
+            padded = n if not pad_block else -(-n // pad_block) * pad_block
+            if pad_block:
+                pos = -(-pos // pad_block) * pad_block
+            lens.append(n); src_off.append(so); dst_off.append(pos)
+            pos += padded
+        dst = torch.full((pos + 64,), 0xEE, dtype=torch.uint8, device="cuda")
+        dev.gather_spans(np.uint64(pool.data_ptr()) + np.array(src_off, dtype=np.uint64), np.array(lens, dtype=np.uint64),
+                         np.array(dst_off, dtype=np.uint64), pad_block, dst)
+        got = dst.cpu().numpy()
+        want = np.full(pos + 64, 0xEE, dtype=np.uint8)
+        for n, so, do in zip(lens, src_off, dst_off):
+            padded = n if not pad_block else -(-n // pad_block) * pad_block
+            want[do:do + n] = host[so:so + n]
+            want[do + n:do + padded] = 0
+        assert np.array_equal(got, want), pad_block
