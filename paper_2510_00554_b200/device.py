@@ -331,15 +331,18 @@ class ModelPlan:
         self.total_bytes = int(lib.snt_model_plan_total_bytes(self._handle))
 
     @classmethod
-    def from_spans(cls, keep: Sequence[object], ptrs: np.ndarray, sizes: np.ndarray, block_size: int) -> "ModelPlan":
-        """Plan over ``device_spans`` output (addresses + byte lengths; ``keep`` holds the owners alive)."""
+    def from_spans(cls, keep: Sequence[object], ptrs: np.ndarray, sizes: np.ndarray, block_size: int,
+                   count: Optional[int] = None) -> "ModelPlan":
+        """Plan over ``device_spans`` output (addresses + byte lengths; ``keep`` holds the owners alive).
+        ``count`` = number of spans when ``keep`` is not one object per span."""
         self = cls.__new__(cls)
         self._handle = ctypes.c_void_p()
         lib = _native.load()
         require_cuda()
         self.tensors = list(keep)
         rc = lib.snt_model_plan_create(ptrs.ctypes.data_as(ctypes.POINTER(ctypes.c_void_p)),
-                                       sizes.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), len(keep), block_size,
+                                       sizes.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)),
+                                       len(keep) if count is None else count, block_size,
                                        _stream(), ctypes.byref(self._handle))
         _native.check(rc, "snt_model_plan_create")
         self.block_size = block_size

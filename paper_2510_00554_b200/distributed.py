@@ -221,13 +221,19 @@ def hash_model_sharded(cfg, model, rank: int, world: int, group=None):
     first = _first_leaves(sizes, bs)
     sp = plan_shards(first[-1], world)
     a, b = sp.leaf_range(rank)
+    # tensors this rank reads (they own leaves of its range) or that already sit on its GPU are described by
+    # their real addresses; the host ones among them are staged together (pinned ring + one device arena);
+    # every other entry keeps its true size but points at a placeholder that no leaf of this rank touches
+    import numpy as np
+
     placeholder = torch.zeros(16, dtype=torch.uint8, device=dev)
-    staged = []
-    for i, (_, buf) in enumerate(model.entries):
-        mine = first[i] < b and first[i + 1] > a
-        on_gpu = isinstance(buf, torch.Tensor) and buf.device.type == "cuda"
-        staged.append(_dev.as_device_bytes(buf, dev) if (mine or on_gpu) else placeholder)
-    plan = _dev.ModelPlan(staged, bs, sizes_override=sizes)
+    wanted = [i for i, (_, buf) in enumerate(model.entries)
+              if (first[i] < b and first[i + 1] > a) or (isinstance(buf, torch.Tensor) and buf.device.type == "cuda")]
+    keep, w_ptrs, _ = _dev.device_spans([model.entries[i][1] for i in wanted], dev)
+    ptrs = np.full(len(sizes), placeholder.data_ptr(), dtype=np.uint64)
+    ptrs[np.asarray(wanted, dtype=np.int64)] = w_ptrs[:len(wanted)]
+    ptrs[np.asarray(sizes) == 0] = 0
+    plan = _dev.ModelPlan.from_spans([keep, placeholder], ptrs, np.asarray(sizes, dtype=np.uint64), bs, count=len(sizes))
     try:
         backend = CudaBackend(plan, cfg.alg.value)
         root = sharded_merkle_root(backend, sp, rank, world, group)

@@ -414,9 +414,8 @@ def per_layer_hash(cfg: HashConfig, model: TensorMap, workers: int = 1) -> Model
         seg_first = [0]
         for c in block_counts:
             seg_first.append(seg_first[-1] + c)
-        plan = _dev.ModelPlan.from_spans([None] * len(live), np.ascontiguousarray(v_ptrs[live]),
-                                         np.ascontiguousarray(v_sizes[live]), bs)
-        plan.tensors = [keep, scratch]                                   # the owners of the spans live as long as the plan
+        plan = _dev.ModelPlan.from_spans([keep, scratch], np.ascontiguousarray(v_ptrs[live]),
+                                         np.ascontiguousarray(v_sizes[live]), bs, count=len(live))
         try:
             hasher = _dev.MerkleModelHasher(plan, alg)
             hasher.run_leaves_only()

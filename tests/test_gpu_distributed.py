@@ -54,6 +54,9 @@ def _worker(rank, world, port, sizes, q):
         h.allreduce()
         out["lattice"] = {k: (v[0].data.hex(), v[1]) for k, v in h.finalize().items()}
         q.put((rank, out))
+    except Exception as exc:                     # surface the failure instead of leaving the peers in a collective
+        q.put((rank, {"error": repr(exc)}))
+        os._exit(1)
     finally:
         dist.destroy_process_group()
 
@@ -70,10 +73,19 @@ def test_ranks_sharing_the_gpu_reproduce_single_gpu_digests(world, porc):
     procs = [ctx.Process(target=_worker, args=(r, world, port, sizes, q)) for r in range(world)]
     for p in procs:
         p.start()
-    results = dict(q.get(timeout=300) for _ in range(world))
-    for p in procs:
-        p.join(60)
-        assert p.exitcode == 0
+    results = {}
+    try:
+        for _ in range(world):
+            rank, out = q.get(timeout=120)
+            assert "error" not in out, (rank, out)
+            results[rank] = out
+        for p in procs:
+            p.join(60)
+            assert p.exitcode == 0
+    finally:
+        for p in procs:                      # a failed rank leaves its peers inside a collective: do not wait for them
+            if p.is_alive():
+                p.kill()
 
     n, declared = 999, [2, 3, 5, 7]
     rng = np.random.default_rng(17)
