@@ -48,6 +48,12 @@ uint32_t max_levels(int alg) {
     return alg == SNT_BLAKE2B ? ReduceShape<ALG_BLAKE2B>::MAX_LEVELS : ReduceShape<ALG_SHA256>::MAX_LEVELS;
 }
 
+// A big level starts with a WIDE launch: WIDE_LEVELS levels over full-width CTAs that each emit
+// 2^(max_levels - WIDE_LEVELS) nodes, so the bulk of the node hashes (7/8 of them) run with every thread
+// busy; the narrowing launches that follow see an 8x smaller level.
+constexpr uint32_t WIDE_LEVELS = 3;
+constexpr uint64_t WIDE_MIN_NODES = 1ull << 18;    // below this the extra launch costs more than it saves (tools/tree_probe.py)
+
 const MerkleConsts& node_consts() {
     static const MerkleConsts c = [] {
         MerkleConsts k;
@@ -182,7 +188,9 @@ size_t snt_merkle_work_bytes(int alg, uint64_t count) {
     // two ping-pong buffers, each able to hold the widest intermediate level:
     // every launch but the last folds max_levels(alg) levels, so the widest
     // intermediate has ceil(count / 2^max_levels) nodes
-    return 2 * static_cast<size_t>(cdiv_shift(count, max_levels(alg)) + 1) * snt_digest_len(alg);
+    // -- or, for a level big enough for the wide first launch, ceil(count / 2^WIDE_LEVELS) nodes
+    const uint64_t widest = count >= WIDE_MIN_NODES ? cdiv_shift(count, WIDE_LEVELS) : cdiv_shift(count, max_levels(alg));
+    return 2 * static_cast<size_t>(widest + 1) * snt_digest_len(alg);
 }
 
 }  // extern "C"
@@ -197,12 +205,12 @@ namespace {
 //                (BLAKE2b / SHA3-256 trees of 800k leaves: -8% / -4%; SHA-256 neutral).
 template <int ALG, int THREADS>
 int launch_reduce_t(const uint8_t* in, uint64_t first, uint64_t n_in, uint64_t level_count, uint32_t levels,
-                    const MerkleConsts& c, uint8_t* out, uint64_t n_out, cudaStream_t s) {
+                    uint32_t glog, const MerkleConsts& c, uint8_t* out, uint64_t n_ctas, cudaStream_t s) {
     static const cudaError_t carve = cudaFuncSetAttribute(
         merkle_reduce_kernel<ALG, THREADS>, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
     (void)carve;
-    merkle_reduce_kernel<ALG, THREADS><<<static_cast<unsigned>(n_out), THREADS, 0, s>>>(
-        in, first, n_in, level_count, levels, c, out);
+    merkle_reduce_kernel<ALG, THREADS><<<static_cast<unsigned>(n_ctas), THREADS, 0, s>>>(
+        in, first, n_in, level_count, levels, glog, c, out);
     SNT_CUDA(cudaGetLastError());
     ++g_launches;
     return SNT_OK;
@@ -210,19 +218,20 @@ int launch_reduce_t(const uint8_t* in, uint64_t first, uint64_t n_in, uint64_t l
 
 template <int ALG>
 int launch_reduce(const uint8_t* in, uint64_t first, uint64_t n_in, uint64_t level_count,
-                  uint32_t levels, const MerkleConsts& c, uint8_t* out, cudaStream_t s) {
-    const uint64_t n_out = cdiv_shift(n_in, levels);
-    if (n_out > 0x7fffffffull) return SNT_ERR_INVALID_INPUT;
-    if (n_out <= 5 * 148) return launch_reduce_t<ALG, 256>(in, first, n_in, level_count, levels, c, out, n_out, s);
-    return launch_reduce_t<ALG, 128>(in, first, n_in, level_count, levels, c, out, n_out, s);
+                  uint32_t levels, uint32_t glog, const MerkleConsts& c, uint8_t* out, cudaStream_t s) {
+    const uint64_t n_ctas = cdiv_shift(n_in, levels + glog);
+    if (n_ctas > 0x7fffffffull) return SNT_ERR_INVALID_INPUT;
+    if (glog == 0 && n_ctas <= 5 * 148)
+        return launch_reduce_t<ALG, 256>(in, first, n_in, level_count, levels, glog, c, out, n_ctas, s);
+    return launch_reduce_t<ALG, 128>(in, first, n_in, level_count, levels, glog, c, out, n_ctas, s);
 }
 
 int launch_reduce_alg(int alg, const uint8_t* in, uint64_t first, uint64_t n_in, uint64_t level_count,
-                      uint32_t levels, const MerkleConsts& c, uint8_t* out, cudaStream_t s) {
+                      uint32_t levels, uint32_t glog, const MerkleConsts& c, uint8_t* out, cudaStream_t s) {
     switch (alg) {
-        case SNT_SHA256: return launch_reduce<ALG_SHA256>(in, first, n_in, level_count, levels, c, out, s);
-        case SNT_BLAKE2B: return launch_reduce<ALG_BLAKE2B>(in, first, n_in, level_count, levels, c, out, s);
-        default: return launch_reduce<ALG_SHA3_256>(in, first, n_in, level_count, levels, c, out, s);
+        case SNT_SHA256: return launch_reduce<ALG_SHA256>(in, first, n_in, level_count, levels, glog, c, out, s);
+        case SNT_BLAKE2B: return launch_reduce<ALG_BLAKE2B>(in, first, n_in, level_count, levels, glog, c, out, s);
+        default: return launch_reduce<ALG_SHA3_256>(in, first, n_in, level_count, levels, glog, c, out, s);
     }
 }
 
@@ -237,7 +246,13 @@ int reduce_chain(int alg, const uint8_t* in, uint64_t first, uint64_t n_in, uint
     const uint8_t* src = in;
     while (levels > 0) {
         const uint32_t cap = max_levels(alg);
-        const uint32_t m = levels < cap ? levels : cap;
+        uint32_t m = levels < cap ? levels : cap;
+        uint32_t glog = 0;
+        if (n_in >= WIDE_MIN_NODES && levels > WIDE_LEVELS && work &&
+            cdiv_shift(n_in, WIDE_LEVELS) * dlen <= half) {          // (a caller with a small workspace keeps the old schedule)
+            m = WIDE_LEVELS;
+            glog = cap - WIDE_LEVELS;
+        }
         const uint64_t n_out = cdiv_shift(n_in, m);
         uint8_t* dst = out;
         if (levels > m) {
@@ -245,7 +260,7 @@ int reduce_chain(int alg, const uint8_t* in, uint64_t first, uint64_t n_in, uint
             dst = work + (flip ? half : 0);
             flip ^= 1;
         }
-        const int rc = launch_reduce_alg(alg, src, first, n_in, level_count, m, c, dst, s);
+        const int rc = launch_reduce_alg(alg, src, first, n_in, level_count, m, glog, c, dst, s);
         if (rc != SNT_OK) return rc;
         src = dst;
         first >>= m;

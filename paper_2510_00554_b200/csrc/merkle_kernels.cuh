@@ -200,18 +200,21 @@ SNT_D void pair_or_pad(uint32_t* left, const uint32_t* right, bool right_exists,
     for (int i = 0; i < A::DW; ++i) left[i] = out[i];
 }
 
-// The reduction of one aligned group of 2^levels inputs starting at global node index `base` (see
-// above); writes the group's single output node to out_digest. Called by every thread of the CTA.
+// The reduction of 2^glog adjacent aligned groups of 2^levels inputs each, starting at global node index
+// `base` (see above); writes one output node per group to out_digests (nodes that do not exist in the tree
+// are skipped). glog = 0 is the narrowing walk down to one node; glog > 0 with few levels is the wide
+// first launch of a big tree: every thread stays busy on every level, so the launch is throughput-bound
+// instead of ending in the latency-bound narrow levels. Called by every thread of the CTA.
 template <int ALG, int THREADS>
 SNT_D void reduce_group(const uint8_t* __restrict__ in, uint64_t first, uint64_t n_in, uint64_t base,
-                        uint64_t level_count, uint32_t levels, const MerkleConsts& c,
-                        uint8_t* __restrict__ out_digest, uint32_t* buf_a, uint32_t* buf_b) {
+                        uint64_t level_count, uint32_t levels, uint32_t glog, const MerkleConsts& c,
+                        uint8_t* __restrict__ out_digests, uint32_t* buf_a, uint32_t* buf_b) {
     using A = AlgTraits<ALG>;
     constexpr int DW = A::DW;
     constexpr int CAP = ReduceShape<ALG>::CAP;
     const uint32_t tid = threadIdx.x;
     const uint64_t in_end = first + n_in;
-    const uint32_t width = 1u << levels;
+    const uint32_t width = 1u << (levels + glog);
 
     // level 0 -> 1 straight from global memory: pair p = inputs base + 2p, base + 2p + 1
     for (uint32_t p = tid; p < (width >> 1); p += THREADS) {
@@ -254,26 +257,30 @@ SNT_D void reduce_group(const uint8_t* __restrict__ in, uint64_t first, uint64_t
         uint32_t* tp = src; src = dst; dst = tp;
         const uint32_t ts = src_stride; src_stride = dst_stride; dst_stride = ts;
     }
-    if (tid == 0) {
-        uint32_t d[DW];
+    const uint64_t out_cnt = ceil_shift(level_count, levels);     // nodes the tree has at the output level
+    const uint64_t obase = base >> levels;
+    for (uint32_t p = tid; p < (1u << glog); p += THREADS) {
+        if (obase + p < out_cnt) {
+            uint32_t d[DW];
 #pragma unroll
-        for (int i = 0; i < DW; ++i) d[i] = src[i * src_stride];
-        store_digest<ALG>(out_digest, d);
+            for (int i = 0; i < DW; ++i) d[i] = src[i * src_stride + p];
+            store_digest<ALG>(out_digests + static_cast<uint64_t>(p) * A::DIGEST_BYTES, d);
+        }
     }
 }
 
 template <int ALG, int THREADS>
 __global__ void __launch_bounds__(THREADS)
 merkle_reduce_kernel(const uint8_t* __restrict__ in, uint64_t first, uint64_t n_in,
-                     uint64_t level_count, uint32_t levels, const __grid_constant__ MerkleConsts c,
+                     uint64_t level_count, uint32_t levels, uint32_t glog, const __grid_constant__ MerkleConsts c,
                      uint8_t* __restrict__ out) {
     using A = AlgTraits<ALG>;
     constexpr int CAP = ReduceShape<ALG>::CAP;
     __shared__ uint32_t buf_a[A::DW * CAP];
     __shared__ uint32_t buf_b[A::DW * CAP / 2];
-    const uint64_t base = first + (static_cast<uint64_t>(blockIdx.x) << levels);   // first input of this CTA
-    reduce_group<ALG, THREADS>(in, first, n_in, base, level_count, levels, c,
-                               out + static_cast<uint64_t>(blockIdx.x) * A::DIGEST_BYTES, buf_a, buf_b);
+    const uint64_t base = first + (static_cast<uint64_t>(blockIdx.x) << (levels + glog));   // first input of this CTA
+    reduce_group<ALG, THREADS>(in, first, n_in, base, level_count, levels, glog, c,
+                               out + (static_cast<uint64_t>(blockIdx.x) << glog) * A::DIGEST_BYTES, buf_a, buf_b);
 }
 
 // One tree per segment (per_layer_hash, model.py:245-253), one CTA per segment, one launch for all
@@ -299,7 +306,7 @@ merkle_reduce_segments_kernel(const uint8_t* __restrict__ in, const uint64_t* __
     }
     uint32_t levels = 0;
     while ((1ull << levels) < count) ++levels;
-    reduce_group<ALG, THREADS>(in + begin * A::DIGEST_BYTES, 0, count, 0, count, levels, c, dst, buf_a, buf_b);
+    reduce_group<ALG, THREADS>(in + begin * A::DIGEST_BYTES, 0, count, 0, count, levels, 0, c, dst, buf_a, buf_b);
 }
 
 }  // namespace snt

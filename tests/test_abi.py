@@ -49,7 +49,8 @@ def test_constants_and_strings(lib):
     assert lib.snt_strerror(0) == b"ok"
     assert b"invalid input" in lib.snt_strerror(-1)
     assert b"unknown" in lib.snt_strerror(-99)
-    assert lib.snt_merkle_work_bytes(0, 799954) == 2 * (782 + 1) * 32
+    assert lib.snt_merkle_work_bytes(0, 79672) == 2 * (78 + 1) * 32               # narrowing launches only
+    assert lib.snt_merkle_work_bytes(0, 799954) == 2 * (99995 + 1) * 32           # wide first launch: count / 8 nodes
     assert lib.snt_merkle_work_bytes(1, 1) == 2 * 2 * 64
 
 
