@@ -51,7 +51,10 @@ uint32_t max_levels(int alg) {
 // A big level starts with a WIDE launch: WIDE_LEVELS levels over full-width CTAs that each emit
 // 2^(max_levels - WIDE_LEVELS) nodes, so the bulk of the node hashes (7/8 of them) run with every thread
 // busy; the narrowing launches that follow see an 8x smaller level.
-constexpr uint32_t WIDE_LEVELS = 3;
+#ifndef SNT_WIDE_LEVELS
+#define SNT_WIDE_LEVELS 3
+#endif
+constexpr uint32_t WIDE_LEVELS = SNT_WIDE_LEVELS;
 constexpr uint64_t WIDE_MIN_NODES = 1ull << 18;    // below this the extra launch costs more than it saves (tools/tree_probe.py)
 
 const MerkleConsts& node_consts() {
