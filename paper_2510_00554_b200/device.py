@@ -111,14 +111,14 @@ class StagingRing:
     @classmethod
     def get(cls, threads: int) -> "StagingRing":
         if cls._instance is None or cls._instance.threads < threads or \
-                cls._instance.bufs[0].numel() != STAGE_SLOT_BYTES:
+                cls._instance.bufs[0].numel() != STAGE_SLOT_BYTES or len(cls._instance.bufs) != STAGE_RING_SLOTS:
             cls._instance = cls(threads)
         return cls._instance
 
     def acquire(self) -> int:
         """Next slot, once the transfer that last used it has completed."""
         slot = self.slot
-        self.slot = (slot + 1) % STAGE_RING_SLOTS
+        self.slot = (slot + 1) % len(self.bufs)
         if self.events[slot] is not None:
             self.events[slot].synchronize()
         return slot

@@ -16,10 +16,12 @@ for arch in ("gpt2", "bert-large"):
     model = pkg.TensorMap(entries)
     cfg = pkg.HashConfig(pkg.Construction.MERKLE, pkg.Strategy.IN_PLACE, pkg.CompressionAlg.SHA256)
     out[arch] = {"bytes": model.total_bytes}
-    for w in (1, 12, 16):                      # workers = staging threads (at least min(8, cores) are used)
-        pkg.hash_model(cfg, model, workers=w)
+    from paper_2510_00554_b200 import device as dv
+    for slot_mb, slots in ((32, 4), (64, 4), (128, 3), (256, 2)):      # transfer size of the staging ring
+        dv.STAGE_SLOT_BYTES, dv.STAGE_RING_SLOTS = slot_mb << 20, slots
+        pkg.hash_model(cfg, model)
         ts = []
         for _ in range(3):
-            t0 = time.perf_counter(); r = pkg.hash_model(cfg, model, workers=w); ts.append(time.perf_counter() - t0)
-        out[arch][f"workers{w}"] = {"ms": round(min(ts) * 1e3, 2), "gbs": round(model.total_bytes / min(ts) / 1e9, 2)}
+            t0 = time.perf_counter(); r = pkg.hash_model(cfg, model); ts.append(time.perf_counter() - t0)
+        out[arch][f"slot{slot_mb}MBx{slots}"] = {"ms": round(min(ts) * 1e3, 2), "gbs": round(model.total_bytes / min(ts) / 1e9, 2)}
 print(json.dumps(out))
