@@ -174,12 +174,6 @@ def _require_nonempty(model: TensorMap) -> None:
         raise InvalidInput("model must contain at least one byte of tensor data")
 
 
-def device_tensors(model: TensorMap) -> List[torch.Tensor]:
-    """Flat uint8 CUDA views (or staged copies) of every entry, in order."""
-    dev = _dev.require_cuda()
-    return [_dev.as_device_bytes(buf, dev) for _, buf in model.entries]
-
-
 def _hash_plan(cfg: HashConfig, plan: _dev.ModelPlan, aux_data_bytes: int = 0) -> ModelDigestResult:
     n = plan.leaf_count
     if cfg.construction is Construction.MERKLE:
@@ -257,14 +251,14 @@ def _inplace_merkle_staged(cfg: HashConfig, model: TensorMap, workers: int = 1) 
         else:
             dst.append(arena[arena_off[i]:arena_off[i] + sizes[i]])
     plan = _dev.ModelPlan(dst, bs)
+    ring = _dev.StagingRing.get(_dev.staging_threads(workers)) if arena_total else None
+    if ring is not None:
+        ring.lock.acquire()                  # one staged hash at a time owns the ring
     try:
         hasher = _dev.MerkleModelHasher(plan, cfg.alg.value)
         main = torch.cuda.current_stream()
         side = torch.cuda.Stream()
         side.wait_stream(main)
-        ring = _dev.StagingRing.get(_dev.staging_threads(workers)) if arena_total else None
-        if ring is not None:
-            ring.lock.acquire()
         # the staging buffer being filled mirrors the arena range [chunk_base, chunk_base + chunk_fill)
         slot, chunk_base, chunk_fill, tasks = -1, 0, 0, []
 
@@ -326,7 +320,7 @@ def _inplace_merkle_staged(cfg: HashConfig, model: TensorMap, workers: int = 1) 
         aux = hasher.leaves.numel() + hasher.work_bytes + (hasher.out.numel() if n_leaves > 1 else 0)
         return ModelDigestResult(root, cfg, n_leaves, aux_digest_bytes=aux)
     finally:
-        if 'ring' in locals() and ring is not None and ring.lock.locked():
+        if ring is not None:
             torch.cuda.synchronize()          # no transfer may still read a staging buffer when the next owner starts
             ring.lock.release()
         plan.close()

@@ -669,6 +669,27 @@ def test_graph_replay_rehashes_current_bytes(pkg, porc):
     assert hasher.out_bytes() == porc.inplace_merkle("sha256", changed, 8192)
 
 
+def test_length_sorted_rows_give_the_same_digests(pkg, corc):
+    from paper_2510_00554_b200 import dataset as dsm, device as dev
+
+    rng = np.random.default_rng(31)
+    n, n_src = 5000, 5
+    lens = rng.integers(0, 1500, size=n).astype(np.uint64)
+    offs = np.zeros(n, dtype=np.uint64)
+    np.cumsum(lens[:-1], out=offs[1:])
+    shard = rng.integers(0, 256, size=int(lens.sum()) + 16, dtype=np.uint8)
+    ids = rng.permutation(n).astype(np.uint64)
+    src = rng.integers(0, n_src, size=n)
+    ds = dsm.DeviceDataset.from_host(shard, offs, lens, ids, src, list(range(n_src)))
+    outs = []
+    for d in (ds, ds.sorted_by_length()):
+        acc = dev.LatticeAccumulator(n_src)
+        d.accumulate(acc)
+        outs.append(acc.digests())
+    assert outs[0] == outs[1]
+    assert bool((ds.sorted_by_length().lengths[1:] >= ds.sorted_by_length().lengths[:-1]).all())
+
+
 def test_gather_spans_any_alignment(pkg):
     """snt_gather_spans against numpy: every source/destination byte phase, zero padding, empty spans, >1 chunk."""
     from paper_2510_00554_b200 import device as dev
