@@ -420,7 +420,10 @@ def per_layer_hash(cfg: HashConfig, model: TensorMap, workers: int = 1) -> Model
             layer_bytes = layers_dev.cpu().numpy().tobytes()
             root = Digest(cfg.alg, root_dev.cpu().numpy().tobytes())
             aux_digest = hasher.leaves.numel() + layers_dev.numel() + hasher.work_bytes
-            aux_data = scratch.numel() if len(ragged) else 0
+            # as in the reference (model.py:231-286), the zero-padded copies of the ragged last blocks are
+            # transient and not counted: aux_data_bytes reports tensor data gathered into a new buffer
+            # (the coalesced strategy), aux_digest_bytes the digest storage
+            aux_data = 0
         finally:
             plan.close()
         layer_digests = {name: Digest(cfg.alg, layer_bytes[i * dlen:(i + 1) * dlen]) for i, name in enumerate(names)}

@@ -669,6 +669,26 @@ def test_graph_replay_rehashes_current_bytes(pkg, porc):
     assert hasher.out_bytes() == porc.inplace_merkle("sha256", changed, 8192)
 
 
+def test_memory_accounting_trend(pkg):
+    """The reference's acceptance criterion 8 (tests/test_acceptance.py:260-275): the coalesced strategy pays one
+    padded copy of the model, per-layer and in-place stay below 2 % of the model size."""
+    from paper_2510_00554_b200 import bench as sbench
+    from paper_2510_00554_b200.model import coalesce_hash, inplace_hash, per_layer_hash
+
+    model = sbench.synthetic_model("bert", scale=0.125, seed=8)            # ~67 MiB, 199 layers
+    total = model.total_bytes
+    assert total >= 64 << 20
+    cfg = lambda strat: pkg.HashConfig(pkg.Construction.MERKLE, strat, pkg.CompressionAlg.SHA256)
+    co = coalesce_hash(cfg(pkg.Strategy.COALESCED), model)
+    bs = co.config.block_size
+    assert co.aux_data_bytes == -(-total // bs) * bs
+    pl = per_layer_hash(cfg(pkg.Strategy.PER_LAYER), model)
+    ip = inplace_hash(cfg(pkg.Strategy.IN_PLACE), model)
+    assert ip.aux_data_bytes == 0 and pl.aux_data_bytes == 0
+    assert pl.aux_bytes <= 0.02 * total and ip.aux_bytes <= 0.02 * total
+    assert len(pl.layer_digests) == 199 and ip.layer_digests is None
+
+
 def test_length_sorted_rows_give_the_same_digests(pkg, corc):
     from paper_2510_00554_b200 import dataset as dsm, device as dev
 
