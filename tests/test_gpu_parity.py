@@ -739,3 +739,38 @@ def test_gather_spans_any_alignment(pkg):
             want[do:do + n] = host[so:so + n]
             want[do + n:do + padded] = 0
         assert np.array_equal(got, want), pad_block
+
+
+def test_hash_model_from_several_threads(pkg, porc):
+    """The hashing entry points are callable from any number of threads: resident models,
+    staged host models (which take turns on the pinned ring) and datasets at the same time."""
+    import threading
+
+    from paper_2510_00554_b200 import device as dv
+
+    rng = np.random.default_rng(77)
+    host = [rng.integers(0, 256, size=s, dtype=np.uint8) for s in ((9 << 20) + 5, 8192 * 700, 333, (12 << 20), 4096 * 3)]
+    want = {a: porc.inplace_merkle(a, [h.tobytes() for h in host], 8192) for a in ALGS}
+    as_bytes = pkg.TensorMap([(f"t{i}", h.tobytes()) for i, h in enumerate(host)])
+    on_gpu = pkg.TensorMap([(f"t{i}", torch.from_numpy(h).cuda()) for i, h in enumerate(host)])
+    errors = []
+
+    def work(k):
+        try:
+            for rep in range(3):
+                alg = ALGS[(k + rep) % 3]
+                cfg = pkg.HashConfig(pkg.Construction.MERKLE, pkg.Strategy.IN_PLACE, _alg(pkg, alg))
+                model = as_bytes if (k + rep) % 2 else on_gpu
+                got = pkg.hash_model(cfg, model, workers=2).model_digest.data
+                if got != want[alg]:
+                    errors.append((k, rep, alg))
+        except Exception as exc:          # noqa: BLE001
+            errors.append((k, repr(exc)))
+
+    threads = [threading.Thread(target=work, args=(k,)) for k in range(6)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join(120)
+    assert not any(t.is_alive() for t in threads), "a hashing thread is stuck"
+    assert errors == []
