@@ -220,9 +220,9 @@ def _inplace_merkle_staged(cfg: HashConfig, model: TensorMap, workers: int = 1) 
     """Host tensors -> device with the copies and the leaf hashing overlapped.
 
     Device buffers are allocated up front (the plan needs their addresses): tensors that are already
-    on the GPU stay where they are, pinned host tensors get their own device buffer and are copied
-    directly, and pageable host buffers are laid out back to back (256-byte aligned) in one device
-    arena and travel through the pinned staging ring in 32 MB transfers. All copies run on a side
+    on the GPU stay where they are; host tensors are laid out back to back (256-byte aligned) in ONE
+    device arena -- pinned ones are copied straight into their slice, pageable ones travel through
+    the pinned staging ring in 32 MB transfers. All copies run on a side
     stream; the leaf kernel for a ~256 MB group of whole tensors is enqueued as soon as its bytes
     have landed, and the tree reduction runs once at the end over the leaf digests.
     """
@@ -231,27 +231,24 @@ def _inplace_merkle_staged(cfg: HashConfig, model: TensorMap, workers: int = 1) 
     entries = model.entries
     sizes = [buffer_nbytes(buf) for _, buf in entries]
     CUDA, PINNED, PAGEABLE = 0, 1, 2
-    kinds, arena_off, arena_total = [], [0] * len(entries), 0
+    kinds, arena_off, arena_total, n_pageable = [], [0] * len(entries), 0, 0
     for i, (_, buf) in enumerate(entries):
         if _is_cuda(buf):
             kinds.append(CUDA)
-        elif isinstance(buf, torch.Tensor) and buf.is_pinned():
-            kinds.append(PINNED)
         else:
-            kinds.append(PAGEABLE)
-            arena_off[i] = arena_total
+            kinds.append(PINNED if isinstance(buf, torch.Tensor) and buf.is_pinned() else PAGEABLE)
+            n_pageable += kinds[-1] == PAGEABLE
+            arena_off[i] = arena_total                      # one device allocation for every staged tensor
             arena_total += -(-sizes[i] // _ARENA_ALIGN) * _ARENA_ALIGN
     arena = torch.empty(max(arena_total, 16), dtype=torch.uint8, device=dev)
     dst: List[torch.Tensor] = []
     for i, (_, buf) in enumerate(entries):
         if kinds[i] == CUDA:
             dst.append(_dev.as_device_bytes(buf, dev))
-        elif kinds[i] == PINNED:
-            dst.append(torch.empty(sizes[i], dtype=torch.uint8, device=dev))
         else:
             dst.append(arena[arena_off[i]:arena_off[i] + sizes[i]])
     plan = _dev.ModelPlan(dst, bs)
-    ring = _dev.StagingRing.get(_dev.staging_threads(workers)) if arena_total else None
+    ring = _dev.StagingRing.get(_dev.staging_threads(workers)) if n_pageable else None
     if ring is not None:
         ring.lock.acquire()                  # one staged hash at a time owns the ring
     try:
@@ -279,6 +276,7 @@ def _inplace_merkle_staged(cfg: HashConfig, model: TensorMap, workers: int = 1) 
         n = len(dst)
         for i, (_, buf) in enumerate(entries):
             if kinds[i] == PINNED and sizes[i]:
+                flush_chunk()        # a ring transfer covers one contiguous arena range: it must not span this slice
                 with torch.cuda.stream(side):
                     dst[i].copy_(_host_tensor(buf), non_blocking=True)
             elif kinds[i] == PAGEABLE and sizes[i]:
