@@ -137,8 +137,8 @@ STAGE_INLINE_MAX_BYTES = 256 << 10     # pieces below this are copied by the cal
 def pageable_to_device(src: np.ndarray, dst: torch.Tensor, workers: int = 1) -> None:
     """Copy a flat uint8 host array into ``dst`` (flat uint8 CUDA tensor) through the pinned ring.
 
-    Enqueues the transfers on the current stream and returns when the last memcpy into a staging
-    buffer is done; the device copy itself completes in stream order.
+    The transfers go to the current stream; the call returns after the last one has completed
+    (the staging buffers are handed back to the ring only when nothing reads them any more).
     """
     ring = StagingRing.get(staging_threads(workers))
     stream = torch.cuda.current_stream()
