@@ -774,3 +774,33 @@ def test_hash_model_from_several_threads(pkg, porc):
         t.join(120)
     assert not any(t.is_alive() for t in threads), "a hashing thread is stuck"
     assert errors == []
+
+
+def test_tensor_larger_than_4_gib(pkg, corc):
+    """Byte offsets past 2^32 inside one tensor and past 2^33 in the model: root, every leaf digest of the far
+    end, lattice digest -- against the C oracle on the same bytes (maximum-size edge of model.py:137-146)."""
+    import os
+
+    from paper_2510_00554_b200 import device as dev
+
+    big = (4 << 30) + 8192 * 3 + 1234                      # one tensor > 4 GiB with a ragged tail
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(5)
+    parts = [torch.randint(0, 256, (big,), dtype=torch.uint8, device="cuda", generator=gen),
+             torch.randint(0, 256, (12345,), dtype=torch.uint8, device="cuda", generator=gen),
+             torch.randint(0, 256, ((1 << 30) + 64,), dtype=torch.uint8, device="cuda", generator=gen)]
+    host = [p.cpu().numpy() for p in parts]
+    tl = corc.TensorList(host)
+    threads = os.cpu_count() or 4
+    n_leaves = tl.leaf_count(8192)
+    assert n_leaves > (1 << 19) and sum(h.size for h in host) > 5 * (1 << 30)
+    plan = dev.ModelPlan(parts, 8192)
+    for alg in ("sha256", "blake2b"):
+        hasher = dev.MerkleModelHasher(plan, alg)
+        hasher.run()
+        want_leaves = corc.inplace_leaves(alg, tl, 8192, threads)
+        assert hasher.leaf_bytes() == want_leaves, alg            # every one of the ~655k leaf digests
+        assert hasher.out_bytes() == corc.inplace_merkle(alg, tl, 8192, threads), alg
+    lat = pkg.HashConfig(pkg.Construction.LATTICE, pkg.Strategy.IN_PLACE, pkg.CompressionAlg.BLAKE2B)
+    got = pkg.hash_model(lat, pkg.TensorMap([(f"t{i}", p) for i, p in enumerate(parts)]))
+    assert got.model_digest.data == corc.inplace_lattice(tl, 8192, threads)
