@@ -46,6 +46,21 @@ const char* snt_last_cuda_error(void);
 uint32_t snt_abi_version(void);
 /* Diagnostic: kernels launched by this library in this process so far. */
 uint64_t snt_debug_launch_count(void);
+/* How snt_merkle_inplace / snt_merkle_leaves schedule their work (process-wide; returns the previous
+ * setting, an unknown value changes nothing). All three give bit-identical results.
+ *   SNT_SCHEDULE_PERSISTENT (default): one persistent CTA per SM, leaves hashed in warp-wide chains with a
+ *       time-sliced tail (csrc/merkle_fused.cuh), then the level-reducer launches. Fastest on every measured
+ *       configuration.
+ *   SNT_SCHEDULE_FUSED: the same leaf scheduling with the tree folded into the SAME launch through
+ *       completion counters -- one launch per hash (needs >= 5 levels and an initialised workspace,
+ *       otherwise falls back to PERSISTENT).
+ *   SNT_SCHEDULE_GRID: one thread per leaf on a plain grid, then the level reducer (round 1's path). */
+typedef enum snt_schedule { SNT_SCHEDULE_PERSISTENT = 0, SNT_SCHEDULE_FUSED = 1, SNT_SCHEDULE_GRID = 2 } snt_schedule;
+int snt_merkle_schedule(int schedule);
+/* Diagnostic: a device buffer of 6 x u64 per SM (zeroed by the caller) into which every persistent CTA of
+ * the fused kernel writes {start ns, last warp exit ns, group reductions done, chain slices run, last
+ * chain finished ns, unused}; NULL (the default) turns tracing off. */
+void snt_debug_fused_trace(void* d_trace);
 /* 32, 64, 32 -- or 0 for an unknown algorithm. */
 uint32_t snt_digest_len(int alg);
 
@@ -68,9 +83,17 @@ void snt_model_plan_destroy(snt_model_plan* plan);
 uint64_t snt_model_plan_leaf_count(const snt_model_plan* plan);
 uint64_t snt_model_plan_total_bytes(const snt_model_plan* plan);
 
-/* Bytes of scratch snt_merkle_inplace / snt_merkle_root need for `count`
- * input digests of `alg`. */
+/* Bytes of scratch snt_merkle_inplace / snt_merkle_root / snt_merkle_reduce_levels need for
+ * `count` leaves or input digests of `alg` (0 for an unknown algorithm). The workspace holds the
+ * reducer's ping-pong levels and, behind them, the state of the fused single-launch kernel
+ * (completion counters, stage nodes, parked chain states). A workspace belongs to one
+ * (alg, count) and to one call at a time. */
 size_t snt_merkle_work_bytes(int alg, uint64_t count);
+
+/* Zero a fresh workspace (asynchronous memset on `stream`). Required once before the first
+ * snt_merkle_inplace that uses it; every call hands the workspace back ready for the next one
+ * (the kernel returns each counter to zero as it consumes it), so launches need no memset. */
+int snt_merkle_work_init(void* d_work, size_t work_bytes, snt_stream_t stream);
 
 /* Leaf stage alone: hash_blocks over the in-place block table (model.py:300-305,
  * merkle.py:93-114). Leaf k of [leaf_begin, leaf_end) is written at
@@ -87,6 +110,9 @@ int snt_merkle_leaves(const snt_model_plan* plan, int alg, uint64_t leaf_begin, 
  *   nodes of that range (multi-GPU sharding; nodes combine with
  *   snt_merkle_root / snt_merkle_reduce_levels into the reference root).
  * d_leaves (may not be NULL) receives every leaf digest of the range.
+ * The workspace must hold snt_merkle_work_bytes(alg, leaf_end - leaf_begin) bytes prepared by
+ * snt_merkle_work_init. Launches: one for the leaves plus one to three for the levels, or a single
+ * one under SNT_SCHEDULE_FUSED (see snt_merkle_schedule).
  */
 int snt_merkle_inplace(const snt_model_plan* plan, int alg, uint64_t leaf_begin,
                        uint64_t leaf_end, uint32_t levels, void* d_leaves, void* d_work,

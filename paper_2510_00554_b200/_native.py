@@ -20,7 +20,8 @@ import os
 LIB_PATH = Path(os.environ.get("SNT_LIB_PATH") or Path(__file__).resolve().parent / "lib" / "libsentinel_b200.so")
 
 SNT_LEVELS_TO_ROOT = 0xFFFFFFFF
-ABI_VERSION = 1
+SCHEDULE_PERSISTENT, SCHEDULE_FUSED, SCHEDULE_GRID = 0, 1, 2
+ABI_VERSION = 2
 
 # name -> (restype, argtypes); mirrors include/sentinel_b200.h one to one
 SIGNATURES = {
@@ -34,7 +35,10 @@ SIGNATURES = {
     "snt_model_plan_destroy": (None, [c_void_p]),
     "snt_model_plan_leaf_count": (c_uint64, [c_void_p]),
     "snt_model_plan_total_bytes": (c_uint64, [c_void_p]),
+    "snt_merkle_schedule": (c_int, [c_int]),
+    "snt_debug_fused_trace": (None, [c_void_p]),
     "snt_merkle_work_bytes": (c_size_t, [c_int, c_uint64]),
+    "snt_merkle_work_init": (c_int, [c_void_p, c_size_t, c_void_p]),
     "snt_gather_chunk_bytes": (c_uint32, []),
     "snt_gather_spans": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_uint32, c_uint64, c_uint32, c_void_p,
                                  c_void_p]),

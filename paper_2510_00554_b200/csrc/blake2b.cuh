@@ -10,6 +10,24 @@
 
 namespace snt {
 
+#define SNT_B2B_SIGMA                                          \
+    {0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15},   \
+    {14, 10, 4, 8, 9, 15, 13, 6, 1, 12, 0, 2, 11, 7, 5, 3},   \
+    {11, 8, 12, 0, 5, 2, 15, 13, 10, 14, 3, 6, 7, 1, 9, 4},   \
+    {7, 9, 3, 1, 13, 12, 11, 14, 2, 6, 5, 10, 4, 0, 15, 8},   \
+    {9, 0, 5, 7, 2, 4, 10, 15, 14, 1, 11, 12, 6, 8, 3, 13},   \
+    {2, 12, 6, 10, 0, 11, 8, 3, 4, 13, 7, 5, 15, 14, 1, 9},   \
+    {12, 5, 1, 15, 14, 13, 4, 10, 0, 7, 6, 3, 9, 2, 8, 11},   \
+    {13, 11, 7, 14, 12, 1, 3, 9, 5, 0, 15, 4, 8, 6, 2, 10},   \
+    {6, 15, 14, 9, 11, 3, 0, 8, 12, 2, 13, 7, 1, 4, 10, 5},   \
+    {10, 2, 8, 4, 7, 6, 1, 5, 15, 11, 9, 14, 3, 12, 13, 0},   \
+    {0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15},   \
+    {14, 10, 4, 8, 9, 15, 13, 6, 1, 12, 0, 2, 11, 7, 5, 3}
+
+#if defined(__CUDACC__)
+__constant__ uint8_t c_b2b_sigma[12][16] = {SNT_B2B_SIGMA};      // for the rolled compression (compress_rolled)
+#endif
+
 struct Blake2b {
     static constexpr int DIGEST_BYTES = 64;
     static constexpr int BLOCK_BYTES = 128;
@@ -75,24 +93,41 @@ struct Blake2b {
     // One compression: t = bytes absorbed so far including this block
     // (messages here are < 2^64 bytes, so the high counter word is zero).
     SNT_HD static void compress(uint64_t h[8], const uint64_t m[16], uint64_t t, bool last) {
-        const uint8_t S[12][16] = {
-            {0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15},
-            {14, 10, 4, 8, 9, 15, 13, 6, 1, 12, 0, 2, 11, 7, 5, 3},
-            {11, 8, 12, 0, 5, 2, 15, 13, 10, 14, 3, 6, 7, 1, 9, 4},
-            {7, 9, 3, 1, 13, 12, 11, 14, 2, 6, 5, 10, 4, 0, 15, 8},
-            {9, 0, 5, 7, 2, 4, 10, 15, 14, 1, 11, 12, 6, 8, 3, 13},
-            {2, 12, 6, 10, 0, 11, 8, 3, 4, 13, 7, 5, 15, 14, 1, 9},
-            {12, 5, 1, 15, 14, 13, 4, 10, 0, 7, 6, 3, 9, 2, 8, 11},
-            {13, 11, 7, 14, 12, 1, 3, 9, 5, 0, 15, 4, 8, 6, 2, 10},
-            {6, 15, 14, 9, 11, 3, 0, 8, 12, 2, 13, 7, 1, 4, 10, 5},
-            {10, 2, 8, 4, 7, 6, 1, 5, 15, 11, 9, 14, 3, 12, 13, 0},
-            {0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15},
-            {14, 10, 4, 8, 9, 15, 13, 6, 1, 12, 0, 2, 11, 7, 5, 3}};
+        const uint8_t S[12][16] = {SNT_B2B_SIGMA};
         uint64_t v0 = h[0], v1 = h[1], v2 = h[2], v3 = h[3], v4 = h[4], v5 = h[5], v6 = h[6], v7 = h[7];
         uint64_t v8 = SNT_B2B_IV0, v9 = SNT_B2B_IV1, v10 = SNT_B2B_IV2, v11 = SNT_B2B_IV3;
         uint64_t v12 = SNT_B2B_IV4 ^ t, v13 = SNT_B2B_IV5;
         uint64_t v14 = last ? ~SNT_B2B_IV6 : SNT_B2B_IV6, v15 = SNT_B2B_IV7;
 #pragma unroll
+        for (int r = 0; r < 12; ++r) {
+            SNT_B2B_G(v0, v4, v8, v12, m[S[r][0]], m[S[r][1]]);
+            SNT_B2B_G(v1, v5, v9, v13, m[S[r][2]], m[S[r][3]]);
+            SNT_B2B_G(v2, v6, v10, v14, m[S[r][4]], m[S[r][5]]);
+            SNT_B2B_G(v3, v7, v11, v15, m[S[r][6]], m[S[r][7]]);
+            SNT_B2B_G(v0, v5, v10, v15, m[S[r][8]], m[S[r][9]]);
+            SNT_B2B_G(v1, v6, v11, v12, m[S[r][10]], m[S[r][11]]);
+            SNT_B2B_G(v2, v7, v8, v13, m[S[r][12]], m[S[r][13]]);
+            SNT_B2B_G(v3, v4, v9, v14, m[S[r][14]], m[S[r][15]]);
+        }
+        h[0] ^= v0 ^ v8;  h[1] ^= v1 ^ v9;  h[2] ^= v2 ^ v10; h[3] ^= v3 ^ v11;
+        h[4] ^= v4 ^ v12; h[5] ^= v5 ^ v13; h[6] ^= v6 ^ v14; h[7] ^= v7 ^ v15;
+    }
+
+    // One compression with the twelve rounds rolled and the message schedule read from a table: ~3 KB
+    // of code instead of 34 KB, for the cold paths that share a kernel with the unrolled leaf loop (tree
+    // nodes) and must not push that loop out of the instruction cache. m is indexed dynamically, so it
+    // lives in local memory.
+    SNT_HD static void compress_rolled(uint64_t h[8], const uint64_t m[16], uint64_t t, bool last) {
+#ifdef __CUDA_ARCH__
+        const uint8_t (*S)[16] = c_b2b_sigma;
+#else
+        static const uint8_t S[12][16] = {SNT_B2B_SIGMA};
+#endif
+        uint64_t v0 = h[0], v1 = h[1], v2 = h[2], v3 = h[3], v4 = h[4], v5 = h[5], v6 = h[6], v7 = h[7];
+        uint64_t v8 = SNT_B2B_IV0, v9 = SNT_B2B_IV1, v10 = SNT_B2B_IV2, v11 = SNT_B2B_IV3;
+        uint64_t v12 = SNT_B2B_IV4 ^ t, v13 = SNT_B2B_IV5;
+        uint64_t v14 = last ? ~SNT_B2B_IV6 : SNT_B2B_IV6, v15 = SNT_B2B_IV7;
+#pragma unroll 1
         for (int r = 0; r < 12; ++r) {
             SNT_B2B_G(v0, v4, v8, v12, m[S[r][0]], m[S[r][1]]);
             SNT_B2B_G(v1, v5, v9, v13, m[S[r][2]], m[S[r][3]]);
@@ -178,6 +213,13 @@ struct Blake2b {
         for (int i = 0; i < 8; ++i) { m[i] = l[i]; m[8 + i] = r[i]; }
         init(out);
         compress(out, m, 128, true);
+    }
+    SNT_HD static void hash_pair_rolled(const uint64_t l[8], const uint64_t r[8], uint64_t out[8]) {
+        uint64_t m[16];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) { m[i] = l[i]; m[8 + i] = r[i]; }
+        init(out);
+        compress_rolled(out, m, 128, true);
     }
 };
 

@@ -67,10 +67,19 @@ struct Blake2bStaged : Blake2b {
     //   T = 1  LE64(index) in front               (LtHash, lattice.py:92-94)
     //   T = 2  LE64(layer) || LE64(block) in front (per-layer lattice, model.py:259)
     template <int T>
-    SNT_HD static void hash_message(uint64_t* bufs, uint64_t tag0, uint64_t tag1, const uint8_t* p, uint64_t len,
-                                    uint64_t h[8]) {
+    SNT_HD static uint64_t block_count(uint64_t len) {
+        const uint64_t total = len + 8ull * T;
+        return total == 0 ? 1 : ((total + 127) >> 7);
+    }
+
+    // Compress message blocks [b0, b1) (clipped to the message's block count) into h, which holds
+    // the chaining value after block b0 - 1 (init(h) for b0 = 0). A message can therefore be hashed
+    // in slices, by different threads if need be: nothing but h travels between slices -- the T
+    // carried words of block b0 are re-read from the message itself.
+    template <int T>
+    SNT_HD static void hash_blocks(uint64_t* bufs, uint64_t tag0, uint64_t tag1, const uint8_t* p, uint64_t len,
+                                   uint64_t b0, uint64_t b1, uint64_t h[8]) {
         static_assert(T >= 0 && T <= B2S_MAX_TAG_WORDS, "unsupported tag width");
-        init(h);
         uint64_t* const buf0 = bufs;
         uint64_t* const buf1 = bufs + B2S_SLOTS * STRIDE;
         const uint64_t nfull = len >> 7;                 // whole 128-byte chunks of data
@@ -78,14 +87,25 @@ struct Blake2bStaged : Blake2b {
         const uint64_t total = len + 8ull * T;
         const uint64_t nblocks = total == 0 ? 1 : ((total + 127) >> 7);
         const uint8_t* q = p + (nfull << 7);             // the ragged tail, r bytes
-        if (nfull > 0) stage_chunk<T>(buf0, p);
+        if (b1 > nblocks) b1 = nblocks;
+        if (b0 >= b1) return;
+        uint64_t* const first = (b0 & 1) ? buf1 : buf0;
+        if (b0 < nfull) stage_chunk<T>(first, p + (b0 << 7));
         commit();
-        if (T >= 1) buf0[0] = tag0;
-        if (T >= 2) buf0[STRIDE] = tag1;
-        for (uint64_t b = 0; b < nblocks; ++b) {
+        if (b0 == 0) {
+            if (T >= 1) first[0] = tag0;
+            if (T >= 2) first[STRIDE] = tag1;
+        } else if (T > 0 && b0 <= nfull) {
+            // resuming: the words carried into block b0 are the last T words of data chunk b0 - 1
+            uint64_t carry[T > 0 ? T : 1];
+            load_words64<(T > 0 ? T : 1)>(p + (b0 << 7) - 8 * T, carry);
+#pragma unroll
+            for (int i = 0; i < T; ++i) first[i * STRIDE] = carry[i];
+        }
+        for (uint64_t b = b0; b < b1; ++b) {
             uint64_t* cur = (b & 1) ? buf1 : buf0;
             uint64_t* nxt = (b & 1) ? buf0 : buf1;
-            if (b + 1 < nfull) stage_chunk<T>(nxt, p + ((b + 1) << 7));
+            if (b + 1 < nfull && b + 1 < b1) stage_chunk<T>(nxt, p + ((b + 1) << 7));
             commit();
             if (b < nfull) {
                 wait_pending<1>();                        // chunk b has landed in slots T..T+15
@@ -106,6 +126,13 @@ struct Blake2bStaged : Blake2b {
             const bool last = b + 1 == nblocks;
             compress(h, m, last ? total : ((b + 1) << 7), last);
         }
+    }
+
+    template <int T>
+    SNT_HD static void hash_message(uint64_t* bufs, uint64_t tag0, uint64_t tag1, const uint8_t* p, uint64_t len,
+                                    uint64_t h[8]) {
+        init(h);
+        hash_blocks<T>(bufs, tag0, tag1, p, len, 0, ~0ull, h);
     }
 };
 

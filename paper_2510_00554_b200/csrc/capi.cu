@@ -3,8 +3,10 @@
 // level-reducer launches. No torch types, no allocation on the hashing path.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <vector>
@@ -12,6 +14,7 @@
 #include "../../include/sentinel_b200.h"
 #include "gather_kernels.cuh"
 #include "lthash_kernels.cuh"
+#include "merkle_fused.cuh"
 #include "merkle_kernels.cuh"
 
 using namespace snt;
@@ -22,6 +25,10 @@ thread_local char g_cuda_err[256] = "";
 
 // diagnostic only: number of kernels this library has launched in this process
 std::atomic<uint64_t> g_launches{0};
+// how snt_merkle_inplace / snt_merkle_leaves schedule their work (snt_merkle_schedule)
+std::atomic<int> g_schedule{SNT_SCHEDULE_PERSISTENT};
+// diagnostic only: device buffer of 6 x u64 per CTA the fused kernel writes its timeline into
+std::atomic<unsigned long long*> g_fused_trace{nullptr};
 
 int cuda_fail(cudaError_t e, const char* where) {
     snprintf(g_cuda_err, sizeof(g_cuda_err), "%s: %s", where, cudaGetErrorString(e));
@@ -55,6 +62,9 @@ uint32_t max_levels(int alg) {
 #define SNT_WIDE_LEVELS 3
 #endif
 constexpr uint32_t WIDE_LEVELS = SNT_WIDE_LEVELS;
+#ifndef SNT_FUSED_MAXW_SHA256
+#define SNT_FUSED_MAXW_SHA256 24
+#endif
 constexpr uint64_t WIDE_MIN_NODES = 1ull << 18;    // below this the extra launch costs more than it saves (tools/tree_probe.py)
 
 const MerkleConsts& node_consts() {
@@ -68,11 +78,61 @@ const MerkleConsts& node_consts() {
     return c;
 }
 
+// SMs of the current device (one persistent CTA each in the fused kernel); 148 when there is no device
+// to ask, so that the size queries of the ABI work on a machine without a GPU.
+int sm_count() {
+    static const int n = [] {
+        int dev = 0, sms = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess ||
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) {
+            cudaGetLastError();
+            return 148;
+        }
+        return sms;
+    }();
+    return n;
+}
+
+// Worker warps per persistent CTA, upper bound per algorithm (registers: 65,536 / (32 * W)).
+constexpr int FUSED_MAXW_SHA256 = SNT_FUSED_MAXW_SHA256;
+constexpr int FUSED_MAXW_WIDE = 16;      // SHA3-256
+constexpr int FUSED_MAXW_BLAKE2B = 8;    // fewer, fatter warps: 34 KB of unrolled rounds per warp position, 128+ registers
+size_t align256(size_t x) { return (x + 255) & ~static_cast<size_t>(255); }
+
+// Workspace of one (algorithm, node count): [ping-pong levels of the multi-launch reducer | completion
+// counters | stage nodes]. The last two belong to the fused kernel; the counters must be zero before
+// its first launch (snt_merkle_work_init) and it hands them back zeroed.
+struct WorkLayout {
+    size_t pingpong, counters_off, counters_bytes, nodes_off, nodes_bytes, total;
+};
+
+size_t pingpong_bytes(int alg, uint64_t count) {
+    // two ping-pong buffers, each able to hold the widest intermediate level:
+    // every launch but the last folds max_levels(alg) levels, so the widest
+    // intermediate has ceil(count / 2^max_levels) nodes
+    // -- or, for a level big enough for the wide first launch, ceil(count / 2^WIDE_LEVELS) nodes
+    const uint64_t widest = count >= WIDE_MIN_NODES ? cdiv_shift(count, WIDE_LEVELS) : cdiv_shift(count, max_levels(alg));
+    return align256(2 * static_cast<size_t>(widest + 1) * snt_digest_len(alg));
+}
+
+WorkLayout work_layout(int alg, uint64_t count) {
+    WorkLayout w;
+    w.pingpong = pingpong_bytes(alg, count);
+    // groups of stage 0 <= ceil(count / 32), every later stage at most halves: < 2 * that + one per stage
+    const size_t n_groups = 2 * static_cast<size_t>(cdiv_shift(count, FUSED_MIN_LEVELS)) + 2 * FUSED_MAX_STAGES;
+    w.counters_off = w.pingpong;
+    w.counters_bytes = align256(n_groups * sizeof(uint32_t));
+    w.nodes_off = w.counters_off + w.counters_bytes;
+    w.nodes_bytes = align256(n_groups * snt_digest_len(alg));
+    w.total = w.nodes_off + w.nodes_bytes;
+    return w;
+}
+
 }  // namespace
 
 struct snt_model_plan {
     uint64_t* d_table = nullptr;     // addr[n] | nbytes[n] | first_leaf[n + 1] | irregular[n_irregular]
-    uint32_t n_irregular = 0;        // leaves that are ragged or not 16-byte aligned (SHA-256 generic path)
+    uint32_t n_irregular = 0;        // leaves of tensors that are not 16-byte aligned (SHA-256 generic path)
     cudaStream_t stream = nullptr;   // the stream the table was allocated and filled on
     std::vector<uint64_t> host;      // staging copy of the table (kept alive until destroy)
     uint32_t n_tensors = 0;
@@ -108,9 +168,18 @@ const char* snt_strerror(int status) {
 
 const char* snt_last_cuda_error(void) { return g_cuda_err; }
 
-uint32_t snt_abi_version(void) { return 1; }
+uint32_t snt_abi_version(void) { return 2; }
 
 uint64_t snt_debug_launch_count(void) { return g_launches.load(); }
+
+int snt_merkle_schedule(int schedule) {
+    const int old = g_schedule.load();
+    if (schedule == SNT_SCHEDULE_PERSISTENT || schedule == SNT_SCHEDULE_FUSED || schedule == SNT_SCHEDULE_GRID)
+        g_schedule.store(schedule);
+    return old;
+}
+
+void snt_debug_fused_trace(void* d_trace) { g_fused_trace.store(static_cast<unsigned long long*>(d_trace)); }
 
 uint32_t snt_digest_len(int alg) {
     switch (alg) {
@@ -143,8 +212,6 @@ int snt_model_plan_create(const void* const* d_tensor_ptrs, const uint64_t* tens
         if (nb && !d_tensor_ptrs[t]) return SNT_ERR_INVALID_INPUT;
         if (addr & 15) {
             for (uint64_t j = 0; j < count; ++j) irregular.push_back(leaves + j);
-        } else if (nb & (block_size - 1)) {
-            irregular.push_back(leaves + count - 1);
         }
         leaves += count;
         total += nb;
@@ -188,12 +255,14 @@ uint64_t snt_model_plan_leaf_count(const snt_model_plan* plan) { return plan ? p
 uint64_t snt_model_plan_total_bytes(const snt_model_plan* plan) { return plan ? plan->total_bytes : 0; }
 
 size_t snt_merkle_work_bytes(int alg, uint64_t count) {
-    // two ping-pong buffers, each able to hold the widest intermediate level:
-    // every launch but the last folds max_levels(alg) levels, so the widest
-    // intermediate has ceil(count / 2^max_levels) nodes
-    // -- or, for a level big enough for the wide first launch, ceil(count / 2^WIDE_LEVELS) nodes
-    const uint64_t widest = count >= WIDE_MIN_NODES ? cdiv_shift(count, WIDE_LEVELS) : cdiv_shift(count, max_levels(alg));
-    return 2 * static_cast<size_t>(widest + 1) * snt_digest_len(alg);
+    if (!valid_alg(alg)) return 0;
+    return work_layout(alg, count).total;
+}
+
+int snt_merkle_work_init(void* d_work, size_t work_bytes, snt_stream_t stream) {
+    if (!d_work || work_bytes == 0) return SNT_ERR_INVALID_INPUT;
+    SNT_CUDA(cudaMemsetAsync(d_work, 0, work_bytes, static_cast<cudaStream_t>(stream)));
+    return SNT_OK;
 }
 
 }  // extern "C"
@@ -244,7 +313,9 @@ int reduce_chain(int alg, const uint8_t* in, uint64_t first, uint64_t n_in, uint
                  uint32_t levels, uint8_t* work, size_t work_bytes, uint8_t* out,
                  const MerkleConsts& c, cudaStream_t s) {
     const uint32_t dlen = snt_digest_len(alg);
-    const size_t half = work_bytes / 2;
+    // only the ping-pong part of a full workspace: what lies behind it belongs to the fused kernel
+    const size_t pp = pingpong_bytes(alg, n_in);
+    const size_t half = (work_bytes < pp ? work_bytes : pp) / 2;
     int flip = 0;
     const uint8_t* src = in;
     while (levels > 0) {
@@ -289,6 +360,110 @@ int launch_leaves(const snt_model_plan* plan, uint64_t begin, uint64_t end, uint
     return SNT_OK;
 }
 
+// The whole hash of leaves [begin, end) down to level `levels` in one launch (merkle_fused.cuh).
+template <int ALG, int MAXW>
+int launch_fused(const snt_model_plan* plan, uint64_t begin, uint64_t end, uint32_t levels, int warps, uint8_t* d_leaves,
+                 uint8_t* work, const WorkLayout& wl, uint8_t* d_out, cudaStream_t s) {
+    constexpr size_t stage_bytes = fused_smem_bytes<ALG, MAXW>();
+    static const cudaError_t attr = cudaFuncSetAttribute(
+        merkle_fused_kernel<ALG, MAXW>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(stage_bytes));
+    if (attr != cudaSuccess) return cuda_fail(attr, "cudaFuncSetAttribute(merkle_fused_kernel)");
+    FusedArgs a;
+    memset(&a, 0, sizeof(a));
+    a.tab = plan->table();
+    a.leaf_begin = begin;
+    a.n = end - begin;
+    if (ALG == ALG_SHA256 && plan->n_irregular) {
+        const uint64_t* irr = plan->host.data() + 3ull * plan->n_tensors + 1;
+        const uint64_t* lo = std::lower_bound(irr, irr + plan->n_irregular, begin);
+        const uint64_t* hi = std::lower_bound(lo, irr + plan->n_irregular, end);
+        a.irregular = plan->d_table + 3ull * plan->n_tensors + 1 + (lo - irr);
+        a.n_irregular = static_cast<uint32_t>(hi - lo);
+    }
+    a.d_leaves = d_leaves;
+    a.trace = g_fused_trace.load();
+    a.flip = getenv("SNT_FUSED_FLIP") ? 1u : 0u;
+    // stages: 8 levels from the leaves, then 6 at a time
+    uint32_t left = levels;
+    uint64_t n_in = a.n;
+    uint32_t* cnt = reinterpret_cast<uint32_t*>(work + wl.counters_off);
+    uint8_t* nodes = work + wl.nodes_off;
+    const uint32_t dlen = AlgTraits<ALG>::DIGEST_BYTES;
+    while (left > 0) {
+        const uint32_t st = a.tree.n_stages++;
+        const uint32_t m = st == 0 ? (left < FUSED_FIRST_STAGE_LEVELS ? left : FUSED_FIRST_STAGE_LEVELS)
+                                   : (left < FUSED_NEXT_STAGE_LEVELS ? left : FUSED_NEXT_STAGE_LEVELS);
+        const uint64_t groups = cdiv_shift(n_in, m);
+        a.tree.m[st] = m;
+        a.tree.n_in[st] = n_in;
+        a.tree.cnt[st] = cnt;
+        a.tree.nodes[st] = left == m ? d_out : nodes;
+        cnt += groups;
+        nodes += groups * dlen;
+        n_in = groups;
+        left -= m;
+    }
+    const uint64_t chains = ((a.n + 31) >> 5) + ((a.n_irregular + 31) >> 5);
+    const uint64_t sms = static_cast<uint64_t>(sm_count());
+    const unsigned grid = static_cast<unsigned>(chains < sms ? chains : sms);
+    if (getenv("SNT_FUSED_NOTREE")) a.tree.n_stages = 0;          // diagnostics: leaf phase alone (no root)
+    merkle_fused_kernel<ALG, MAXW><<<grid, warps * 32, stage_bytes, s>>>(a, plan->consts);
+    SNT_CUDA(cudaGetLastError());
+    ++g_launches;
+    return SNT_OK;
+}
+
+// Worker warps per persistent CTA: a multiple of four (one per scheduler) not above the chains every SM
+// gets, so that the time-sliced tail keeps every scheduler equally busy.
+int fused_warps(const snt_model_plan* plan, int alg, uint64_t begin, uint64_t end, int maxw) {
+    uint64_t chains = (end - begin + 31) >> 5;
+    if (alg == SNT_SHA256) chains += (plan->n_irregular + 31) >> 5;      // an upper bound is good enough here
+    const uint64_t sms = static_cast<uint64_t>(sm_count());
+    const uint64_t grid = chains < sms ? chains : sms;
+    int warps = static_cast<int>((chains / (grid ? grid : 1)) & ~3ull);
+    if (const char* force = getenv("SNT_FUSED_WARPS")) warps = atoi(force) & ~3;
+    return warps < 4 ? 4 : (warps > maxw ? maxw : warps);
+}
+
+// Can the fused kernel take this job? It needs the full workspace, a tree deep enough for a chain of 32
+// leaves to sit inside one first-stage group, and no more stages than FusedTree holds.
+bool fused_applies(uint64_t n, uint32_t levels, size_t work_bytes, const WorkLayout& wl) {
+    if (levels < FUSED_MIN_LEVELS || work_bytes < wl.total || n == 0) return false;
+    const uint32_t rest = levels > FUSED_FIRST_STAGE_LEVELS ? levels - FUSED_FIRST_STAGE_LEVELS : 0;
+    return 1 + (rest + FUSED_NEXT_STAGE_LEVELS - 1) / FUSED_NEXT_STAGE_LEVELS <= FUSED_MAX_STAGES;
+}
+
+// The persistent kernel for [begin, end): leaves only (levels = 0) or with the tree folded in.
+int fused_dispatch(const snt_model_plan* plan, int alg, uint64_t begin, uint64_t end, uint32_t levels, uint8_t* leaves,
+                   uint8_t* work, const WorkLayout& wl, uint8_t* out, cudaStream_t s) {
+    const int warps = fused_warps(plan, alg, begin, end, alg == SNT_SHA256 ? FUSED_MAXW_SHA256
+                                                          : alg == SNT_BLAKE2B ? FUSED_MAXW_BLAKE2B : FUSED_MAXW_WIDE);
+    switch (alg) {
+        case SNT_SHA256:
+            // two builds of the SHA-256 kernel: up to 16 warps with the registers ptxas likes best (~96),
+            // up to 24 warps capped at 80 registers for the models that have that many chains per SM
+            if (warps <= 16) return launch_fused<ALG_SHA256, 16>(plan, begin, end, levels, warps, leaves, work, wl, out, s);
+            return launch_fused<ALG_SHA256, FUSED_MAXW_SHA256>(plan, begin, end, levels, warps, leaves, work, wl, out, s);
+        case SNT_BLAKE2B:
+            return launch_fused<ALG_BLAKE2B, FUSED_MAXW_BLAKE2B>(plan, begin, end, levels, warps, leaves, work, wl, out, s);
+        default:
+            return launch_fused<ALG_SHA3_256, FUSED_MAXW_WIDE>(plan, begin, end, levels, warps, leaves, work, wl, out, s);
+    }
+}
+
+// The leaf stage alone, scheduled as asked: the persistent time-sliced kernel with the tree switched off, or
+// the plain one-thread-per-leaf grid.
+int leaf_stage(const snt_model_plan* plan, int alg, uint64_t begin, uint64_t end, uint8_t* leaves, cudaStream_t s) {
+    if (g_schedule.load() == SNT_SCHEDULE_GRID) {
+        switch (alg) {
+            case SNT_SHA256: return launch_leaves<ALG_SHA256>(plan, begin, end, leaves, s);
+            case SNT_BLAKE2B: return launch_leaves<ALG_BLAKE2B>(plan, begin, end, leaves, s);
+            default: return launch_leaves<ALG_SHA3_256>(plan, begin, end, leaves, s);
+        }
+    }
+    return fused_dispatch(plan, alg, begin, end, 0, leaves, nullptr, WorkLayout{}, nullptr, s);
+}
+
 template <int ALG>
 int launch_blocks(const uint8_t* base, const uint64_t* off, const uint64_t* len, uint64_t n,
                   uint8_t* out, cudaStream_t s) {
@@ -331,13 +506,7 @@ int snt_merkle_leaves(const snt_model_plan* plan, int alg, uint64_t leaf_begin, 
     if (!plan || !d_leaves) return SNT_ERR_INVALID_INPUT;
     if (!valid_alg(alg)) return SNT_ERR_CONFIG;
     if (leaf_begin >= leaf_end || leaf_end > plan->n_leaves) return SNT_ERR_INVALID_INPUT;
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
-    uint8_t* leaves = static_cast<uint8_t*>(d_leaves);
-    switch (alg) {
-        case SNT_SHA256: return launch_leaves<ALG_SHA256>(plan, leaf_begin, leaf_end, leaves, s);
-        case SNT_BLAKE2B: return launch_leaves<ALG_BLAKE2B>(plan, leaf_begin, leaf_end, leaves, s);
-        default: return launch_leaves<ALG_SHA3_256>(plan, leaf_begin, leaf_end, leaves, s);
-    }
+    return leaf_stage(plan, alg, leaf_begin, leaf_end, static_cast<uint8_t*>(d_leaves), static_cast<cudaStream_t>(stream));
 }
 
 int snt_merkle_inplace(const snt_model_plan* plan, int alg, uint64_t leaf_begin, uint64_t leaf_end,
@@ -357,12 +526,13 @@ int snt_merkle_inplace(const snt_model_plan* plan, int alg, uint64_t leaf_begin,
     }
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     uint8_t* leaves = static_cast<uint8_t*>(d_leaves);
-    int rc;
-    switch (alg) {
-        case SNT_SHA256: rc = launch_leaves<ALG_SHA256>(plan, leaf_begin, leaf_end, leaves, s); break;
-        case SNT_BLAKE2B: rc = launch_leaves<ALG_BLAKE2B>(plan, leaf_begin, leaf_end, leaves, s); break;
-        default: rc = launch_leaves<ALG_SHA3_256>(plan, leaf_begin, leaf_end, leaves, s); break;
+    if (d_work && g_schedule.load() == SNT_SCHEDULE_FUSED) {
+        const WorkLayout wl = work_layout(alg, leaf_end - leaf_begin);
+        if (fused_applies(leaf_end - leaf_begin, levels, work_bytes, wl))
+            return fused_dispatch(plan, alg, leaf_begin, leaf_end, levels, leaves, static_cast<uint8_t*>(d_work), wl,
+                                  static_cast<uint8_t*>(d_out), s);
     }
+    const int rc = leaf_stage(plan, alg, leaf_begin, leaf_end, leaves, s);
     if (rc != SNT_OK) return rc;
     const uint32_t dlen = snt_digest_len(alg);
     if (levels == 0) {

@@ -117,16 +117,18 @@ struct Sha3_256 {
         return v;
     }
 
-    // Whole message; out = first four lanes = the 32 digest bytes little-endian.
-    // One loop, one permute call site: full rate blocks, then the padded tail
-    // (0x06 after the last byte, 0x80 in the last rate byte).
-    SNT_HD static void hash_message(const uint8_t* p, uint64_t len, uint64_t out[4]) {
-        uint64_t a[25];
-#pragma unroll
-        for (int i = 0; i < 25; ++i) a[i] = 0;
+    // Number of permutations a message of `len` bytes takes: its full rate blocks plus the padded tail.
+    SNT_HD static uint64_t block_count(uint64_t len) { return len / RATE_BYTES + 1; }
+
+    // Absorb rate blocks [u0, u1) (clipped to block_count(len)) into the sponge state a. One loop,
+    // one permute call site: full rate blocks, then the padded tail (0x06 after the last byte,
+    // 0x80 in the last rate byte). Slices of one message may run in different threads: the 25
+    // lanes are all that travels.
+    SNT_HD static void absorb_blocks(uint64_t a[25], const uint8_t* p, uint64_t len, uint64_t u0, uint64_t u1) {
         const uint64_t nfull = len / RATE_BYTES;
         const uint32_t rem = static_cast<uint32_t>(len - nfull * RATE_BYTES);   // 0..135
-        for (uint64_t blk = 0; blk <= nfull; ++blk) {
+        if (u1 > nfull + 1) u1 = nfull + 1;
+        for (uint64_t blk = u0; blk < u1; ++blk) {
             const uint8_t* q = p + blk * RATE_BYTES;
             if (blk < nfull) {
                 uint32_t w[2 * RATE_LANES];
@@ -145,6 +147,14 @@ struct Sha3_256 {
             }
             permute(a);
         }
+    }
+
+    // Whole message; out = first four lanes = the 32 digest bytes little-endian.
+    SNT_HD static void hash_message(const uint8_t* p, uint64_t len, uint64_t out[4]) {
+        uint64_t a[25];
+#pragma unroll
+        for (int i = 0; i < 25; ++i) a[i] = 0;
+        absorb_blocks(a, p, len, 0, ~0ull);
 #pragma unroll
         for (int i = 0; i < 4; ++i) out[i] = a[i];
     }

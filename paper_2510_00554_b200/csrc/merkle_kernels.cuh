@@ -1,6 +1,6 @@
-// Merkle kernels: leaf hashing (one thread per leaf, fragmented tensors hashed
-// where they lie) and the level reducer (thread-local subtree, then warp
-// shuffles, then one shared-memory hop).
+// Merkle kernels of the multi-launch path: leaf hashing (one thread per leaf, fragmented tensors hashed
+// where they lie) and the level reducer (level by level through shared memory with the active threads
+// compacted). The single-launch path (merkle_fused.cuh) reuses the per-thread pieces defined here.
 //
 // Reference behaviour reproduced:
 //   leaf stage   merkle.py:93-114 (hash_blocks) over model.py:137-146 (BlockTable)
@@ -25,27 +25,26 @@ constexpr int REDUCE_THREADS = 256;       // default CTA size of the level reduc
 
 // ---- leaf hashing -----------------------------------------------------------
 
-// SHA-256 of a full leaf whose length is a multiple of 64 and whose address is
-// 16-byte aligned: 4 x LDG.128 per compression with the next block's loads
-// issued before the current block's rounds, then the constant padding block.
-SNT_HD void sha256_leaf_aligned(const uint8_t* __restrict__ p, uint32_t nblk,
-                               const uint32_t* __restrict__ pad_kw, uint32_t s[8], const Sha256::One& one = Sha256::One()) {
-    Sha256::init(s);
-    U4 q0 = ld128(p), q1 = ld128(p + 16), q2 = ld128(p + 32), q3 = ld128(p + 48);
+// SHA-256 blocks [b0, b1) of a leaf at a 16-byte aligned address: 4 x LDG.128 per 64-byte block, the next
+// block's loads issued before the current block's rounds.
+SNT_HD void sha256_blocks_aligned(const uint8_t* __restrict__ p, uint32_t b0, uint32_t b1, uint32_t s[8],
+                                  const Sha256::One& one = Sha256::One()) {
+    if (b0 >= b1) return;
+    const uint8_t* q = p + (static_cast<size_t>(b0) << 6);
+    U4 q0 = ld128(q), q1 = ld128(q + 16), q2 = ld128(q + 32), q3 = ld128(q + 48);
 #pragma unroll 1
-    for (uint32_t b = 0; b < nblk; ++b) {
+    for (uint32_t b = b0; b < b1; ++b) {
         uint32_t w[16];
         w[0] = bswap32(q0.x);  w[1] = bswap32(q0.y);  w[2] = bswap32(q0.z);  w[3] = bswap32(q0.w);
         w[4] = bswap32(q1.x);  w[5] = bswap32(q1.y);  w[6] = bswap32(q1.z);  w[7] = bswap32(q1.w);
         w[8] = bswap32(q2.x);  w[9] = bswap32(q2.y);  w[10] = bswap32(q2.z); w[11] = bswap32(q2.w);
         w[12] = bswap32(q3.x); w[13] = bswap32(q3.y); w[14] = bswap32(q3.z); w[15] = bswap32(q3.w);
-        if (b + 1 < nblk) {
+        if (b + 1 < b1) {
             const uint8_t* n = p + (static_cast<size_t>(b + 1) << 6);
             q0 = ld128(n); q1 = ld128(n + 16); q2 = ld128(n + 32); q3 = ld128(n + 48);
         }
         Sha256::compress(s, w, one);
     }
-    Sha256::compress_const(s, pad_kw, one);
 }
 
 template <int ALG>
@@ -71,16 +70,6 @@ SNT_D void load_digest(const uint8_t* in, uint32_t* d) {
     }
 }
 
-// One thread per leaf of [leaf_begin, leaf_end); digest k is written at
-// d_leaves + (k - leaf_begin) * DIGEST_BYTES.
-//
-// SHA-256 splits the leaves in two classes at plan time. "Regular" leaves (full
-// block, 16-byte aligned -- all but a few hundred of them) take the fast path in
-// the main part of the grid; a warp's irregular lanes simply sit that launch
-// out, so one ragged leaf no longer drags its 31 neighbours through the generic
-// path. The irregular leaves (ragged tensor tails, tensors at odd addresses)
-// are listed in `irregular` and hashed by the first `irr_ctas` CTAs of the same
-// grid with the generic path, concurrently with the rest.
 // Dynamic shared memory a leaf-hashing CTA needs: BLAKE2b prefetches its message through two
 // staging buffers per thread (blake2b_staged.cuh); the other algorithms load straight to registers.
 template <int ALG>
@@ -104,13 +93,52 @@ SNT_D void hash_one_leaf(const uint8_t* p, uint64_t len, const MerkleConsts& c, 
     }
 }
 
-// The generic path is kept out of line so that it does not take part in the register
-// allocation and instruction scheduling of the regular-leaf loop.
-__device__ __noinline__ void sha256_leaf_generic(const uint8_t* p, uint64_t len, uint32_t one_u, uint32_t one_v,
-                                                 uint32_t d[8]) {
-    Sha256::hash_message(p, len, d, Sha256::One(one_u, one_v));
+// The paths that are not the aligned block loop are kept out of line so that they do not take part in
+// the register allocation and instruction scheduling of that loop.
+//   sha256_leaf_generic  a leaf at an address that is not 16-byte aligned (tensor views at odd offsets)
+//   sha256_finish_cold   the closing blocks of an aligned leaf that is shorter than the block size
+//                        (the ragged last block of a tensor); a full leaf closes with the constant
+//                        padding block instead (Sha256::compress_const)
+__device__ __noinline__ void sha256_finish_cold(const uint8_t* t, uint32_t rem, uint64_t len, uint32_t one_u,
+                                                uint32_t one_v, uint32_t s[8]) {
+    Sha256::finish(t, rem, len, s, Sha256::One(one_u, one_v));
 }
 
+__device__ __noinline__ void sha256_leaf_generic(const uint8_t* p, uint64_t len, uint32_t one_u, uint32_t one_v,
+                                                 uint32_t d[8]) {
+    Sha256::init(d);
+    const uint64_t nfull = len >> 6;
+    const Sha256::One one(one_u, one_v);
+    for (uint64_t b = 0; b < nfull; ++b) {
+        uint32_t w[16];
+        load_words<16>(p + (b << 6), w);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) w[i] = bswap32(w[i]);
+        Sha256::compress(d, w, one);
+    }
+    sha256_finish_cold(p + (nfull << 6), static_cast<uint32_t>(len & 63), len, one_u, one_v, d);
+}
+
+// Close an aligned SHA-256 leaf after its full 64-byte blocks: the constant padding block when the leaf
+// is a whole block, the closing blocks built from its tail bytes otherwise.
+SNT_D void sha256_close_leaf(const LeafRef& leaf, uint32_t block_shift, const MerkleConsts& c, const Sha256::One& one,
+                             uint32_t s[8]) {
+    if (leaf.len == (1ull << block_shift)) {
+        Sha256::compress_const(s, c.sha256_pad_leaf, one);
+    } else {
+        sha256_finish_cold(leaf.ptr + ((leaf.len >> 6) << 6), static_cast<uint32_t>(leaf.len & 63), leaf.len, one.u, one.v, s);
+    }
+}
+
+// One thread per leaf of [leaf_begin, leaf_end); digest k is written at
+// d_leaves + (k - leaf_begin) * DIGEST_BYTES.
+//
+// SHA-256 splits the leaves in two classes at plan time. "Regular" leaves (16-byte aligned address --
+// in practice all of them: allocators align tensors far more strictly) run the aligned block loop in the
+// main part of the grid, a ragged last block of a tensor simply with fewer blocks and its own closing
+// blocks. Leaves of tensors that sit at odd addresses (views at byte offsets) are listed in `irregular`
+// and hashed by the first `irr_ctas` CTAs of the same grid with the generic path, concurrently with the
+// rest; a warp's irregular lanes sit the main part out.
 template <int ALG>
 __global__ void __launch_bounds__(LEAF_THREADS, (ALG == ALG_SHA256) ? SNT_LEAF_MINB : 1)
 merkle_leaf_kernel(const TensorTable tab, const __grid_constant__ MerkleConsts c,
@@ -133,10 +161,10 @@ merkle_leaf_kernel(const TensorTable tab, const __grid_constant__ MerkleConsts c
         const uint64_t k = leaf_begin + static_cast<uint64_t>(blockIdx.x - irr_ctas) * LEAF_THREADS + threadIdx.x;
         if (k >= leaf_end) return;
         const LeafRef leaf = locate_leaf(tab, k);
-        const bool regular = leaf.len == (1ull << tab.block_shift) &&
-                             (reinterpret_cast<uintptr_t>(leaf.ptr) & 15) == 0;
-        if (!regular) return;                              // hashed by the irregular CTAs
-        sha256_leaf_aligned(leaf.ptr, 1u << (tab.block_shift - 6), c.sha256_pad_leaf, d, one);
+        if (reinterpret_cast<uintptr_t>(leaf.ptr) & 15) return;   // hashed by the irregular CTAs
+        Sha256::init(d);
+        sha256_blocks_aligned(leaf.ptr, 0, static_cast<uint32_t>(leaf.len >> 6), d, one);
+        sha256_close_leaf(leaf, tab.block_shift, c, one, d);
         store_digest<ALG>(d_leaves + (k - leaf_begin) * A::DIGEST_BYTES, d);
     } else {
         const uint64_t k = leaf_begin + static_cast<uint64_t>(blockIdx.x) * LEAF_THREADS + threadIdx.x;

@@ -19,6 +19,22 @@
 
 namespace snt {
 
+#define SNT_SHA256_K                                                                            \
+    0x428a2f98u, 0x71374491u, 0xb5c0fbcfu, 0xe9b5dba5u, 0x3956c25bu, 0x59f111f1u, 0x923f82a4u, \
+    0xab1c5ed5u, 0xd807aa98u, 0x12835b01u, 0x243185beu, 0x550c7dc3u, 0x72be5d74u, 0x80deb1feu, \
+    0x9bdc06a7u, 0xc19bf174u, 0xe49b69c1u, 0xefbe4786u, 0x0fc19dc6u, 0x240ca1ccu, 0x2de92c6fu, \
+    0x4a7484aau, 0x5cb0a9dcu, 0x76f988dau, 0x983e5152u, 0xa831c66du, 0xb00327c8u, 0xbf597fc7u, \
+    0xc6e00bf3u, 0xd5a79147u, 0x06ca6351u, 0x14292967u, 0x27b70a85u, 0x2e1b2138u, 0x4d2c6dfcu, \
+    0x53380d13u, 0x650a7354u, 0x766a0abbu, 0x81c2c92eu, 0x92722c85u, 0xa2bfe8a1u, 0xa81a664bu, \
+    0xc24b8b70u, 0xc76c51a3u, 0xd192e819u, 0xd6990624u, 0xf40e3585u, 0x106aa070u, 0x19a4c116u, \
+    0x1e376c08u, 0x2748774cu, 0x34b0bcb5u, 0x391c0cb3u, 0x4ed8aa4au, 0x5b9cca4fu, 0x682e6ff3u, \
+    0x748f82eeu, 0x78a5636fu, 0x84c87814u, 0x8cc70208u, 0x90befffau, 0xa4506cebu, 0xbef9a3f7u, \
+    0xc67178f2u
+
+#if defined(__CUDACC__)
+__constant__ uint32_t c_sha256_k[64] = {SNT_SHA256_K};      // for the rolled compression (compress_rolled)
+#endif
+
 struct Sha256 {
     static constexpr int DIGEST_BYTES = 32;
     static constexpr int STATE_WORDS = 8;     // 32-bit words carried between compressions
@@ -77,17 +93,6 @@ struct Sha256 {
         s[4] = 0x510e527fu; s[5] = 0x9b05688cu; s[6] = 0x1f83d9abu; s[7] = 0x5be0cd19u;
     }
 
-#define SNT_SHA256_K                                                                            \
-    0x428a2f98u, 0x71374491u, 0xb5c0fbcfu, 0xe9b5dba5u, 0x3956c25bu, 0x59f111f1u, 0x923f82a4u, \
-    0xab1c5ed5u, 0xd807aa98u, 0x12835b01u, 0x243185beu, 0x550c7dc3u, 0x72be5d74u, 0x80deb1feu, \
-    0x9bdc06a7u, 0xc19bf174u, 0xe49b69c1u, 0xefbe4786u, 0x0fc19dc6u, 0x240ca1ccu, 0x2de92c6fu, \
-    0x4a7484aau, 0x5cb0a9dcu, 0x76f988dau, 0x983e5152u, 0xa831c66du, 0xb00327c8u, 0xbf597fc7u, \
-    0xc6e00bf3u, 0xd5a79147u, 0x06ca6351u, 0x14292967u, 0x27b70a85u, 0x2e1b2138u, 0x4d2c6dfcu, \
-    0x53380d13u, 0x650a7354u, 0x766a0abbu, 0x81c2c92eu, 0x92722c85u, 0xa2bfe8a1u, 0xa81a664bu, \
-    0xc24b8b70u, 0xc76c51a3u, 0xd192e819u, 0xd6990624u, 0xf40e3585u, 0x106aa070u, 0x19a4c116u, \
-    0x1e376c08u, 0x2748774cu, 0x34b0bcb5u, 0x391c0cb3u, 0x4ed8aa4au, 0x5b9cca4fu, 0x682e6ff3u, \
-    0x748f82eeu, 0x78a5636fu, 0x84c87814u, 0x8cc70208u, 0x90befffau, 0xa4506cebu, 0xbef9a3f7u, \
-    0xc67178f2u
 
     // One compression. w[16] holds the block as big-endian-decoded words and
     // is overwritten by the rolling schedule.
@@ -102,6 +107,30 @@ struct Sha256 {
                 w[t & 15] = add_fma(x, y, one.u);
             }
             round_fma(a, b, c, d, e, f, g, h, K[t], &w[t & 15], one);
+        }
+        s[0] += a; s[1] += b; s[2] += c; s[3] += d; s[4] += e; s[5] += f; s[6] += g; s[7] += h;
+    }
+
+    // One compression with the rounds rolled four times over a 16-round body and the round constants
+    // read from a table: a quarter of the code of compress() (7 KB instead of 26 KB). For the cold paths
+    // that share a kernel with the unrolled leaf loop (tree nodes, closing blocks, leaves at odd addresses)
+    // and must not push that loop out of the instruction cache.
+    SNT_HD static void compress_rolled(uint32_t s[8], uint32_t w[16]) {
+#ifdef __CUDA_ARCH__
+        const uint32_t* K = c_sha256_k;
+#else
+        static const uint32_t K[64] = {SNT_SHA256_K};
+#endif
+        uint32_t a = s[0], b = s[1], c = s[2], d = s[3], e = s[4], f = s[5], g = s[6], h = s[7];
+#pragma unroll 1
+        for (int t0 = 0; t0 < 64; t0 += 16) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                if (t0) w[i] += ssig1(w[(i + 14) & 15]) + w[(i + 9) & 15] + ssig0(w[(i + 1) & 15]);
+                const uint32_t t1 = h + bsig1(e) + ch(e, f, g) + K[t0 + i] + w[i];
+                const uint32_t t2 = bsig0(a) + maj(a, b, c);
+                h = g; g = f; f = e; e = d + t1; d = c; c = b; b = a; a = t1 + t2;
+            }
         }
         s[0] += a; s[1] += b; s[2] += c; s[3] += d; s[4] += e; s[5] += f; s[6] += g; s[7] += h;
     }
@@ -135,45 +164,49 @@ struct Sha256 {
         for (int t = 0; t < 64; ++t) kw[t] = K[t] + w[t];
     }
 
-    // Whole message at p[0..len), any alignment, any length (generic path).
-    // One loop, one compress call site: data blocks first, then the one or
-    // two padding blocks (0x80, zeros, 64-bit big-endian bit length).
-    SNT_HD static void hash_message(const uint8_t* p, uint64_t len, uint32_t s[8], const One& one = One()) {
-        init(s);
-        const uint64_t nfull = len >> 6;
-        const uint32_t rem = static_cast<uint32_t>(len & 63);
-        const uint64_t nblocks = nfull + (rem >= 56 ? 2 : 1);
-        const uint8_t* t = p + (nfull << 6);
+    // The one or two closing blocks of a message of `len` bytes whose last `rem` (< 64) bytes start at t
+    // (any alignment): the tail bytes, 0x80, zeros, the 64-bit big-endian bit length.
+    SNT_HD static void finish(const uint8_t* t, uint32_t rem, uint64_t len, uint32_t s[8], const One& one = One()) {
         const uint64_t bits = len << 3;
-        for (uint64_t b = 0; b < nblocks; ++b) {
+        const int nb = rem >= 56 ? 2 : 1;
+#pragma unroll 1
+        for (int b = 0; b < nb; ++b) {
             uint32_t w[16];
-            if (b < nfull) {
-                load_words<16>(p + (b << 6), w);
 #pragma unroll
-                for (int i = 0; i < 16; ++i) w[i] = bswap32(w[i]);
-            } else {
-                const bool first_pad = (b == nfull);
+            for (int i = 0; i < 16; ++i) {
+                uint32_t v = 0;
+                if (b == 0) {
 #pragma unroll
-                for (int i = 0; i < 16; ++i) {
-                    uint32_t v = 0;
-                    if (first_pad) {
-#pragma unroll
-                        for (int j = 0; j < 4; ++j) {
-                            const uint32_t idx = 4 * i + j;
-                            uint32_t byte = tail_byte(t, idx, rem);
-                            if (idx == rem) byte = 0x80u;
-                            v = (v << 8) | byte;
-                        }
+                    for (int j = 0; j < 4; ++j) {
+                        const uint32_t idx = 4 * i + j;
+                        uint32_t byte = tail_byte(t, idx, rem);
+                        if (idx == rem) byte = 0x80u;
+                        v = (v << 8) | byte;
                     }
-                    w[i] = v;
                 }
-                if (b == nblocks - 1) {
-                    w[14] = static_cast<uint32_t>(bits >> 32);
-                    w[15] = static_cast<uint32_t>(bits);
-                }
+                w[i] = v;
+            }
+            if (b == nb - 1) {
+                w[14] = static_cast<uint32_t>(bits >> 32);
+                w[15] = static_cast<uint32_t>(bits);
             }
             compress(s, w, one);
         }
+    }
+
+    // Whole message at p[0..len), any alignment, any length (generic path): the full 64-byte blocks,
+    // then the closing blocks.
+    SNT_HD static void hash_message(const uint8_t* p, uint64_t len, uint32_t s[8], const One& one = One()) {
+        init(s);
+        const uint64_t nfull = len >> 6;
+        for (uint64_t b = 0; b < nfull; ++b) {
+            uint32_t w[16];
+            load_words<16>(p + (b << 6), w);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) w[i] = bswap32(w[i]);
+            compress(s, w, one);
+        }
+        finish(p + (nfull << 6), static_cast<uint32_t>(len & 63), len, s, one);
     }
 
     // Tree node: H(left || right) where both children are given as state
@@ -190,6 +223,20 @@ struct Sha256 {
         compress_const(s, pad64_kw, one);
 #pragma unroll
         for (int i = 0; i < 8; ++i) out[i] = s[i];
+    }
+
+    // hash_pair with the rolled compression: the second block is the padding of a 64-byte message.
+    SNT_HD static void hash_pair_rolled(const uint32_t l[8], const uint32_t r[8], uint32_t out[8]) {
+        uint32_t w[16];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) { w[i] = l[i]; w[8 + i] = r[i]; }
+        init(out);
+        compress_rolled(out, w);
+        w[0] = 0x80000000u;
+#pragma unroll
+        for (int i = 1; i < 15; ++i) w[i] = 0;
+        w[15] = 512;
+        compress_rolled(out, w);
     }
 
     // Digest bytes <-> state words (big-endian words).

@@ -401,7 +401,8 @@ class MerkleModelHasher:
         self.n_out = 1 if levels is None else -(-count // (1 << levels))
         self.leaves = torch.empty(count * self.dlen, dtype=torch.uint8, device=dev)
         self.work_bytes = merkle_work_bytes(alg, count)
-        self.work = torch.empty(max(self.work_bytes, 16), dtype=torch.uint8, device=dev)
+        # zeroed once: the fused kernel keeps its completion counters at zero between launches
+        self.work = torch.zeros(max(self.work_bytes, 16), dtype=torch.uint8, device=dev)
         self.out_padded = torch.zeros(max(self.n_out, out_capacity or 0) * self.dlen, dtype=torch.uint8, device=dev)
         self.out = self.out_padded[:self.n_out * self.dlen]
 

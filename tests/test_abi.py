@@ -44,14 +44,19 @@ def test_header_cites_the_reference_interface():
 
 
 def test_constants_and_strings(lib):
-    assert lib.snt_abi_version() == 1
+    assert lib.snt_abi_version() == 2
     assert [lib.snt_digest_len(a) for a in (0, 1, 2, 3)] == [32, 64, 32, 0]
     assert lib.snt_strerror(0) == b"ok"
     assert b"invalid input" in lib.snt_strerror(-1)
     assert b"unknown" in lib.snt_strerror(-99)
-    assert lib.snt_merkle_work_bytes(0, 79672) == 2 * (78 + 1) * 32               # narrowing launches only
-    assert lib.snt_merkle_work_bytes(0, 799954) == 2 * (99995 + 1) * 32           # wide first launch: count / 8 nodes
-    assert lib.snt_merkle_work_bytes(1, 1) == 2 * 2 * 64
+    # workspace = ping-pong levels of the multi-launch reducer + counters, stage nodes and parked chain
+    # states of the fused kernel; sized from (alg, count) alone, no device needed
+    assert lib.snt_merkle_work_bytes(0, 79672) >= 2 * (78 + 1) * 32 + 4 * (79672 // 32)
+    assert lib.snt_merkle_work_bytes(0, 799954) >= 2 * (99995 + 1) * 32 + 4 * (799954 // 32)
+    assert lib.snt_merkle_work_bytes(0, 799954) > lib.snt_merkle_work_bytes(0, 79672) > lib.snt_merkle_work_bytes(0, 1) > 0
+    assert lib.snt_merkle_work_bytes(1, 1000) > lib.snt_merkle_work_bytes(0, 1000)      # 64-byte digests, 16-word states
+    assert lib.snt_merkle_work_bytes(7, 1000) == 0
+    assert lib.snt_merkle_work_init(None, 0, None) == -1
 
 
 def test_argument_validation_before_any_cuda_call(lib):

@@ -1,0 +1,164 @@
+"""GPU parity of the persistent kernel (csrc/merkle_fused.cuh) under all three schedules of
+``snt_merkle_schedule``: PERSISTENT (time-sliced leaf chains, then the level-reducer launches -- the default),
+FUSED (the tree folded into the same launch through completion counters) and GRID (round 1's one thread per
+leaf grid).
+
+Every case is checked bit-exact against the C oracle (leaf digests and root), the three schedules against each
+other, and the fused launch against itself on repeated launches over the same workspace (the kernel must hand
+every completion counter back at zero).
+"""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+ALGS = ["sha256", "blake2b", "sha3-256"]
+
+
+@pytest.fixture(scope="module")
+def dev():
+    from paper_2510_00554_b200 import _native, device
+
+    assert torch.cuda.is_available(), "gpu tests need a CUDA device"
+    _native.load()
+    return device
+
+
+def _ragged_model(seed, n_tensors, max_bytes, arena_bytes, odd_addresses=True):
+    """Tensors carved out of one device arena at arbitrary byte offsets: ragged tails, empty tensors,
+    tensors smaller than a block, unaligned addresses. Returns (device views, host arrays)."""
+    rng = np.random.default_rng(seed)
+    host_arena = rng.integers(0, 256, size=arena_bytes, dtype=np.uint8)
+    arena = torch.from_numpy(host_arena).cuda()
+    views, host, pos = [], [], 0
+    for i in range(n_tensors):
+        kind = rng.integers(0, 6)
+        if kind == 0:
+            size = 0
+        elif kind == 1:
+            size = int(rng.integers(1, 300))
+        elif kind == 2:
+            size = int(rng.integers(1, 8)) * 8192                       # whole blocks
+        else:
+            size = int(rng.integers(1, max_bytes))
+        align = 1 if (odd_addresses and rng.integers(0, 3) == 0) else 16
+        pos = -(-pos // align) * align + (int(rng.integers(1, 16)) if align == 1 else 0)
+        if pos + size > arena_bytes:
+            break
+        views.append(arena[pos:pos + size])
+        host.append(host_arena[pos:pos + size])
+        pos += size
+    return views, host
+
+
+def _both_paths(dev, plan, alg, begin=0, end=None, levels=None):
+    """(leaf digests, output) under every schedule; asserts they agree. Returns the pair and the number of
+    launches the fused schedule took."""
+    from paper_2510_00554_b200 import _native
+
+    lib = _native.load()
+    results = {}
+    fused_launches = None
+    try:
+        for schedule in (_native.SCHEDULE_FUSED, _native.SCHEDULE_PERSISTENT, _native.SCHEDULE_GRID):
+            lib.snt_merkle_schedule(schedule)
+            hasher = dev.MerkleModelHasher(plan, alg, begin, end, levels)
+            launches = lib.snt_debug_launch_count()
+            hasher.run()
+            if schedule == _native.SCHEDULE_FUSED:
+                fused_launches = lib.snt_debug_launch_count() - launches
+            results[schedule] = (hasher.leaf_bytes(), hasher.out_bytes())
+            if schedule == _native.SCHEDULE_FUSED:
+                for _ in range(2):                           # counters are back at zero: same answer again
+                    hasher.leaves.zero_()
+                    hasher.out.zero_()
+                    hasher.run()
+                    assert (hasher.leaf_bytes(), hasher.out_bytes()) == results[schedule]
+    finally:
+        lib.snt_merkle_schedule(_native.SCHEDULE_PERSISTENT)
+    got = results[_native.SCHEDULE_FUSED]
+    for schedule, other in results.items():
+        assert got[0] == other[0], f"leaf digests differ between the fused schedule and schedule {schedule}"
+        assert got[1] == other[1], f"tree output differs between the fused schedule and schedule {schedule}"
+    return got, fused_launches
+
+
+@pytest.mark.parametrize("alg", ALGS)
+@pytest.mark.parametrize("block_size", [64, 1024, 8192])
+def test_ragged_models_fused_vs_oracle(dev, corc, alg, block_size):
+    budget = {64: 3 << 20, 1024: 24 << 20, 8192: 96 << 20}[block_size]
+    views, host = _ragged_model(100 + block_size, 400, max(budget // 40, 4096), budget)
+    plan = dev.ModelPlan(views, block_size)
+    (leaves, root), launches = _both_paths(dev, plan, alg)
+    tl = corc.TensorList(host)
+    threads = corc.threads_default()
+    want_leaves = corc.inplace_leaves(alg, tl, block_size, threads)
+    assert leaves == want_leaves
+    assert root == corc.merkle_root(alg, want_leaves, plan.leaf_count, threads)
+    assert launches == 1, "the fused schedule is one launch per hash"
+
+
+@pytest.mark.parametrize("alg", ALGS)
+def test_tree_shapes_around_group_boundaries(dev, corc, alg):
+    """Leaf counts around every stage boundary (32-leaf chains, 256-leaf groups, 2^14-node stages) at a
+    small block size: single ragged groups, one node past a full group, exact powers of two."""
+    bs = 64
+    counts = [32, 33, 255, 256, 257, 511, 513, 1000, 4096, 16383, 16384, 16385, 16384 + 257, 40000]
+    rng = np.random.default_rng(7)
+    for n in counts:
+        data = rng.integers(0, 256, size=n * bs - int(rng.integers(0, bs)), dtype=np.uint8)
+        views = [torch.from_numpy(data).cuda()]
+        plan = dev.ModelPlan(views, bs)
+        assert plan.leaf_count == n
+        (leaves, root), _ = _both_paths(dev, plan, alg)
+        tl = corc.TensorList([data])
+        want_leaves = corc.inplace_leaves(alg, tl, bs, 4)
+        assert leaves == want_leaves, n
+        assert root == corc.merkle_root(alg, want_leaves, n, 4), n
+
+
+@pytest.mark.parametrize("alg", ALGS)
+def test_shard_ranges_forced_levels(dev, porc, alg):
+    """levels = k over aligned leaf ranges (the multi-GPU shard rule) through the fused launch."""
+    bs = 64
+    n = 9000
+    rng = np.random.default_rng(17)
+    data = rng.integers(0, 256, size=n * bs - 5, dtype=np.uint8)
+    plan = dev.ModelPlan([torch.from_numpy(data).cuda()], bs)
+    host = data.tobytes()
+    dl = porc.DIGEST_LEN[alg]
+    all_leaves = b"".join(porc.h(alg, host[i * bs:(i + 1) * bs]) for i in range(n))
+    for k in (5, 6, 8, 9, 10, 13):
+        width = 1 << k
+        ranges = [(0, n), (width, min(n, 3 * width)), ((n // width) * width, n)]
+        for begin, end in ranges:
+            if begin >= end:
+                continue
+            (leaves, out), _ = _both_paths(dev, plan, alg, begin, end, k)
+            assert leaves == all_leaves[begin * dl:end * dl], (k, begin, end)
+            assert out == porc.reduce_levels_forced(alg, all_leaves[begin * dl:end * dl], begin, end - begin, n, k), \
+                (k, begin, end)
+
+
+def test_time_sliced_tail_is_exercised(dev, corc):
+    """More chains than worker warps on every SM with a remainder: the parked-state FIFO runs."""
+    bs = 8192
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    n = sms * 32 * 17 + 32 * 5 + 3                      # 17 chains and a bit per SM
+    rng = np.random.default_rng(23)
+    data = torch.from_numpy(rng.integers(0, 256, size=n * bs - 100, dtype=np.uint8)).cuda()
+    a, b, c = bs * 1000 + 64, bs * 1300 + 65, bs * 1600 + 80
+    # ragged tails, one tensor at an odd address (~300 irregular SHA-256 leaves), the rest regular
+    pieces = [data[:a], data[a:b], data[b:c], data[c:]]
+    host = [p.cpu().numpy() for p in pieces]
+    for alg in ALGS:
+        plan = dev.ModelPlan(pieces, bs)
+        (leaves, root), launches = _both_paths(dev, plan, alg)
+        tl = corc.TensorList(host)
+        threads = corc.threads_default()
+        want_leaves = corc.inplace_leaves(alg, tl, bs, threads)
+        assert leaves == want_leaves, alg
+        assert root == corc.merkle_root(alg, want_leaves, plan.leaf_count, threads), alg
+        assert launches == 1

@@ -59,22 +59,46 @@ def test_every_alignment_and_ragged_length(hc):
 def test_node_hash_and_zero_padding(hc):
     rng = random.Random(2)
     for name, (aid, fn, dl) in ALG.items():
-        left, right = rng.randbytes(dl), rng.randbytes(dl)
-        out = (ctypes.c_uint8 * dl)()
-        hc.hc_pair(aid, left, right, out)
-        assert bytes(out) == fn(left + right).digest()
-        hc.hc_pair(aid, left, bytes(dl), out)
-        assert bytes(out) == fn(left + bytes(dl)).digest()
+        for small in (0, 1):                 # unrolled and rolled formulations of the node hash
+            left, right = rng.randbytes(dl), rng.randbytes(dl)
+            out = (ctypes.c_uint8 * dl)()
+            hc.hc_pair(aid, left, right, out, small)
+            assert bytes(out) == fn(left + right).digest()
+            hc.hc_pair(aid, left, bytes(dl), out, small)
+            assert bytes(out) == fn(left + bytes(dl)).digest()
 
 
-def test_sha256_aligned_fast_path_and_pad_schedule(hc):
+def test_sha256_aligned_path_sliced_and_ragged(hc):
+    """The aligned block loop resumed mid-leaf, the constant padding block, and the closing blocks of a ragged leaf."""
     rng = random.Random(3)
-    for n in (64, 128, 1024, 8192, 65536):
+    for n in (64, 128, 1024, 8192, 65536, 1, 55, 56, 63, 65, 100, 119, 120, 127, 6400, 8191, 3072 + 57):
         data = rng.randbytes(n)
         keep, p = _aligned(data, 0)
-        out = (ctypes.c_uint8 * 32)()
-        hc.hc_sha256_aligned(ctypes.c_void_p(p), ctypes.c_uint64(n), out)
-        assert bytes(out) == hashlib.sha256(data).digest(), n
+        for split in (0, 1, 7, (n >> 6) // 2, n >> 6):
+            out = (ctypes.c_uint8 * 32)()
+            hc.hc_sha256_aligned(ctypes.c_void_p(p), ctypes.c_uint64(n), ctypes.c_uint32(split), out)
+            assert bytes(out) == hashlib.sha256(data).digest(), (n, split)
+
+
+def test_sliced_blake2b_and_sha3_carry_nothing_but_the_state(hc):
+    """hash_blocks / absorb_blocks in slices (what a parked chain resumes from) == the one-shot digest."""
+    rng = random.Random(8)
+    lengths = [0, 1, 127, 128, 129, 135, 136, 137, 255, 256, 257, 271, 272, 273, 1000, 3072, 8191, 8192, 8193]
+    for n in lengths + [rng.randint(0, 9000) for _ in range(40)]:
+        for shift in (0, 8, rng.randint(1, 15)):
+            data = rng.randbytes(n)
+            keep, p = _aligned(data, shift)
+            for slice_blocks in (1, 3, 16, 1000):
+                out = (ctypes.c_uint8 * 32)()
+                hc.hc_sha3_sliced(ctypes.c_void_p(p), ctypes.c_uint64(n), ctypes.c_uint32(slice_blocks), out)
+                assert bytes(out) == hashlib.sha3_256(data).digest(), (n, shift, slice_blocks)
+                for t in (0, 1, 2):
+                    t0, t1 = rng.getrandbits(64), rng.getrandbits(64)
+                    out = (ctypes.c_uint8 * 64)()
+                    hc.hc_blake2b_sliced(t, ctypes.c_uint64(t0), ctypes.c_uint64(t1), ctypes.c_void_p(p),
+                                         ctypes.c_uint64(n), ctypes.c_uint32(slice_blocks), out)
+                    tag = [b"", struct.pack("<Q", t0), struct.pack("<QQ", t0, t1)][t]
+                    assert bytes(out) == hashlib.blake2b(tag + data).digest(), (t, n, shift, slice_blocks)
 
 
 def test_tagged_blake2b_layouts(hc, golden):
