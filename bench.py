@@ -1,20 +1,26 @@
 #!/usr/bin/env python
-"""Benchmark of the hashing hot path on B200 (contract: see the repo brief / DESIGN.md).
+"""Benchmark of the hashing hot path on B200 (contract: see the repo brief / DESIGN.md section 6).
 
     python bench.py --gpus N --steps K --warmup W            # this repo's CUDA engine
-    python bench.py --impl reference --gpus N --steps K ...  # the reference's CPU path (oracle port)
+    python bench.py --impl reference --gpus N --steps K ...  # the UNMODIFIED reference package on the host cores
 
-One "step" = one pass of the hot path over one batch of synthetic input:
-the SHA-256 Merkle in-place hash of a random-init fp32 GPT2-XL state dict
-(581 tensors, 6,552,089,600 bytes, 799,954 leaves of 8 KiB) down to the root.
-`value` is whole-job throughput in GB/s (10^9 tensor bytes per second) with the
-tensors resident in HBM; `e2e` is the same metric through the public
-`hash_model(cfg, TensorMap(host tensors))` call, host->device copies included.
-The CIFAR10-shaped LtHash dataset metric (samples/s) rides along under "dataset".
+One "step" = one pass of the hot path over one batch of synthetic input: the SHA-256 Merkle in-place hash
+of a random-init fp32 GPT2-XL state dict (581 tensors, 6,552,089,600 bytes, 799,954 leaves of 8 KiB) down
+to the root. `value` is whole-job throughput in GB/s (10^9 tensor bytes per second) with the tensors
+resident in HBM; `e2e` is the same metric through the public `hash_model(cfg, TensorMap(host tensors))`
+call, host->device copies included. Every other BASELINE.json configuration rides along under "configs"
+(GPT-2 small SHA-256; BERT-large and VGG19 x {BLAKE2b, SHA3-256}; CIFAR10-shaped LtHash; the
+hellaswag-shaped pool of config 5), each with its own roofline and CPU reference.
 
-Multi-GPU (torchrun, one rank per GPU): the model is replicated, each rank hashes a
-contiguous run of 1024-leaf shards, one all-gather of shard roots, every rank
-finishes the top of the tree -> strong scaling of one model hash.
+Parity is checked before any time is printed: the reference package
+(`oracle/_ref/sentinel`, staged by build()) hashes the D2H copy of the very bytes the GPU hashed; roots,
+leaf digests (sampled) and per-source lattice digests must be bit-identical or the run aborts.
+
+Multi-GPU (`--gpus N`, N > 1): when not already under torchrun the script re-launches itself with one
+rank per GPU (`python -m torch.distributed.run`); the model is replicated, each rank hashes a
+contiguous run of 1024-leaf shards, one NCCL all-gather of shard roots, every rank finishes the top of
+the tree -> strong scaling of one model hash. NCCL_DEBUG=INFO is set so the communicator lines land on
+stderr.
 """
 
 from __future__ import annotations
@@ -22,6 +28,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -35,11 +42,20 @@ sys.path.insert(0, str(ROOT))
 METRIC = "gpt2xl_sha256_merkle_inplace_hash_throughput"
 UNIT = "GB/s"
 WORKLOAD = "GPT2-XL (1.5B, random-init fp32, 581 tensors, 6.55 GB) SHA-256 Merkle in-place hash, block 8192"
-SHA256_OPS_PER_LEAF = 180_600      # 128 x 1400 + 904 + byte swaps, 8 KiB leaf
-# ALU-pipe instructions the leaf kernel actually executes per 8 KiB leaf (SASS of merkle_leaf_kernel<0>:
-# 576 SHF.W + 96 SHF + 352 LOP3 + 16 PRMT per data block, 384 SHF.W + 256 LOP3 for the constant padding
-# block); every addition runs as an IMAD on the FMA pipe (616 per data block).
-SHA256_ALU_INSTR_PER_LEAF = 128 * 1040 + 640
+BLOCK = 8192
+# Root of the seed-0 GPT2-XL state dict of shapes.synthetic_state_dict generated on a CUDA device (torch's
+# Philox stream): both arms hash these very bytes, the reference arm checks its root against this pin.
+PINNED_ROOTS = {("gpt2-xl", "sha256"): "d11fec86b65f2f91ce084c01ba14010fcec9e4a2f07bd2497ba4aca7fdfa9d41"}
+
+# Instructions one thread issues per 8 KiB leaf, from the SASS of the persistent kernel
+# (profiles/r2_sass_report.txt, tools/sass_report.py): the aligned SHA-256 loop is 1,046 ALU-pipe + 603
+# FMA-pipe (IMAD) instructions per 64-byte block, the constant padding block 640 + 512; one BLAKE2b block
+# (128 B, message staging included) 2,066 + 226; one Keccak round 181 ALU, 24 rounds + ~110 of absorb per
+# 136-byte block, no additions.
+ALU_PER_LEAF = {"sha256": 128 * 1046 + 640, "blake2b": 64 * 2066, "sha3-256": 61 * (24 * 181 + 110)}
+FMA_PER_LEAF = {"sha256": 128 * 603 + 512, "blake2b": 64 * 226, "sha3-256": 0}
+LT_ALU_PER_BLOCK, LT_FMA_PER_BLOCK = 2150, 276        # lthash kernel, one 128-byte BLAKE2b block of a sample
+SHA256_OPS_PER_LEAF = 180_600                         # SURVEY.md section 8(d) op model (128 x 1400 + 904 + swaps)
 
 
 def parse_args():
@@ -53,9 +69,10 @@ def parse_args():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-dataset", action="store_true")
+    ap.add_argument("--no-configs", action="store_true")
     ap.add_argument("--no-intpeak", action="store_true")
-    ap.add_argument("--cpu-sample-mb", type=int, default=1024)
+    ap.add_argument("--reference-budget-s", type=float, default=200.0,
+                    help="--impl reference: wall-clock budget of the timed passes; above it a prefix of the model is hashed")
     return ap.parse_args()
 
 
@@ -111,86 +128,383 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
-# ----------------------------------------------------------------------------- CPU side
+# ----------------------------------------------------------------------------- the reference package (CPU)
 
-def host_model_sample(arch: str, max_bytes: int, seed: int = 0):
-    """The first tensors of the architecture's state dict up to ~max_bytes, random bytes (host)."""
-    import numpy as np
+def load_reference():
+    """The unmodified reference package staged under oracle/_ref by build(); None if it did not travel."""
+    ref_dir = ROOT / "oracle" / "_ref"
+    if not (ref_dir / "sentinel" / "__init__.py").exists():
+        try:
+            from paper_2510_00554_b200 import build
 
-    from paper_2510_00554_b200 import shapes
+            build.stage_reference()
+        except Exception:
+            pass
+    if not (ref_dir / "sentinel" / "__init__.py").exists():
+        return None
+    if str(ref_dir) not in sys.path:
+        sys.path.insert(0, str(ref_dir))
+    import sentinel
 
-    rng = np.random.default_rng(seed)
-    tensors, total = [], 0
-    for _name, shape, alias in shapes.ARCHITECTURES[arch]():
-        if alias is not None:
-            continue
-        nbytes = shapes.numel(shape) * 4
-        if tensors and total + nbytes > max_bytes:
+    return sentinel
+
+
+def host_views(sd):
+    """Host copies of the device tensors: [(name, uint8 numpy array)], tied entries shared."""
+    import torch
+
+    seen, out = {}, []
+    for name, t in sd:
+        key = t.data_ptr()
+        if key not in seen:
+            seen[key] = t.reshape(-1).view(torch.uint8).cpu().numpy()
+        out.append((name, seen[key]))
+    return out
+
+
+def reference_model(ref, host):
+    return ref.TensorMap([(name, memoryview(arr)) for name, arr in host])
+
+
+def reference_cfg(ref, alg):
+    return ref.HashConfig(ref.Construction.MERKLE, ref.Strategy.IN_PLACE, ref.CompressionAlg.from_name(alg), BLOCK)
+
+
+def timed_cpu(fn, repeats=1):
+    best, out = None, None
+    for _ in range(repeats):
+        t0 = time.perf_counter()
+        out = fn()
+        dt = time.perf_counter() - t0
+        best = dt if best is None else min(best, dt)
+    return best, out
+
+
+def reference_leaf_digests(ref, alg, host, max_bytes):
+    """hash_blocks(...).data of the reference over the first tensors (<= max_bytes): bytes, leaf count, tensor count."""
+    entries, total = [], 0
+    for name, arr in host:
+        if entries and total + arr.size > max_bytes:
             break
-        tensors.append(rng.integers(0, 256, size=nbytes, dtype=np.uint8))
-        total += nbytes
-    return tensors, total
+        entries.append((name, memoryview(arr)))
+        total += arr.size
+    tm = ref.TensorMap(entries)
+    table = ref.BlockTable.build(tm, BLOCK)
+    views = [memoryview(buf) for _, buf in tm.entries]
+    blocks = [views[t][off:off + ln] for _, t, off, ln in table.rows]
+    buf = ref.hash_blocks(ref.CompressionAlg.from_name(alg), blocks, os.cpu_count() or 1)
+    return bytes(buf.data), len(blocks), len(entries)
 
 
-def cpu_baseline_python(alg: str, tensors, total: int, workers: int, repeats: int = 1):
-    """The oracle port of the reference (hashlib + thread pool), GB/s."""
-    from oracle import sentinel_oracle as orc
-
-    best = None
-    for _ in range(repeats):
-        t0 = time.perf_counter()
-        orc.inplace_merkle(alg, tensors, 8192, workers=workers)
-        dt = time.perf_counter() - t0
-        best = dt if best is None else min(best, dt)
-    return total / best / 1e9, best
-
-
-def cpu_baseline_c(alg: str, tensors, total: int, threads: int, repeats: int = 2):
-    from oracle import c_oracle
-
-    tl = c_oracle.TensorList(tensors)
-    best = None
-    for _ in range(repeats):
-        t0 = time.perf_counter()
-        c_oracle.inplace_merkle(alg, tl, 8192, threads)
-        dt = time.perf_counter() - t0
-        best = dt if best is None else min(best, dt)
-    return total / best / 1e9, best
-
+# ----------------------------------------------------------------------------- --impl reference
 
 def run_reference(args):
-    """--impl reference: the reference's CPU path (its oracle port) on this box's host cores."""
+    """The reference's own CPU implementation of the path, all host threads, on the bytes the GPU arm hashes."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    import torch
+
+    from paper_2510_00554_b200 import shapes
+
     cores = os.cpu_count() or 1
-    sample_bytes = min(args.cpu_sample_mb, 512) << 20
-    tensors, total = host_model_sample(args.arch, sample_bytes)
-    for _ in range(min(args.warmup, 1)):
-        cpu_baseline_python(args.alg, tensors, total, cores)
+    ref = load_reference()
+    on_cuda = torch.cuda.is_available()
+    device = torch.device("cuda", 0) if on_cuda else torch.device("cpu")
+    sd = shapes.synthetic_state_dict(args.arch, device, seed=0)
+    host = host_views(sd)
+    total_bytes = sum(arr.size for _, arr in host)
+    n_leaves = sum(-(-arr.size // BLOCK) for _, arr in host)
+    del sd
+    if on_cuda:
+        torch.cuda.empty_cache()
+    if ref is not None:
+        kind = "reference"
+        cfg = reference_cfg(ref, args.alg)
+
+        def one_pass(h):
+            return ref.hash_model(cfg, reference_model(ref, h), workers=cores).model_digest.data.hex()
+    else:                                   # the staged copy did not travel: the oracle port stands in, and says so
+        kind = "port"
+        from oracle import sentinel_oracle as orc
+
+        def one_pass(h):
+            return orc.inplace_merkle(args.alg, [a for _, a in h], BLOCK, workers=cores).hex()
+
+    # first (untimed) pass: the root check, and the per-pass cost that decides between the full model and a prefix
+    t_first, root = timed_cpu(lambda: one_pass(host))
+    pinned = PINNED_ROOTS.get((args.arch, args.alg)) if on_cuda else None
+    root_ok = None if pinned is None else (root == pinned)
+    if root_ok is False:
+        print(f"bench.py: reference root {root} differs from the pinned root {pinned}", file=sys.stderr)
+    passes = max(0, args.warmup - 1) + args.steps
+    sample_host, sample_bytes, sample_note = host, total_bytes, "the full state dict"
+    if passes * t_first > args.reference_budget_s:
+        want = total_bytes * args.reference_budget_s / (passes * t_first)
+        sample_host, sample_bytes = [], 0
+        for name, arr in host:
+            if sample_host and sample_bytes + arr.size > want:
+                break
+            sample_host.append((name, arr))
+            sample_bytes += arr.size
+        sample_note = f"the first {len(sample_host)} tensors ({sample_bytes / 1e6:.0f} MB) of the state dict"
+    for _ in range(max(0, args.warmup - 1)):
+        one_pass(sample_host)
     times = []
-    for _ in range(max(1, min(args.steps, 10))):
-        _, dt = cpu_baseline_python(args.alg, tensors, total, cores)
+    for _ in range(args.steps):
+        dt, _ = timed_cpu(lambda: one_pass(sample_host))
         times.append(dt)
     dt = statistics.median(times)
-    value = total / dt / 1e9
-    c_gbs, _ = cpu_baseline_c(args.alg, tensors, total, cores)
-    sample = (f"first {len(tensors)} tensors of the {args.arch} state dict ({total / 1e6:.0f} MB, random bytes), "
-              f"Python/hashlib port with a {cores}-thread pool, median of {len(times)} passes")
+    value = sample_bytes / dt / 1e9
+    sample = (f"{'reference package sentinel.hash_model' if kind == 'reference' else 'oracle port'}"
+              f"(MERKLE, IN_PLACE, {args.alg}, 8192, workers={cores}) over {sample_note}, "
+              f"bytes = D2H copy of the GPU arm's tensors" + ("" if on_cuda else " (no CUDA device: CPU generator)"))
+    headline = (args.arch, args.alg) == ("gpt2-xl", "sha256")
     line = {
-        "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": args.gpus,
-        "steps": len(times), "warmup": min(args.warmup, 1), "ms_per_step": round(dt * 1e3, 3),
+        "impl": "reference",
+        "metric": METRIC if headline else f"{args.arch}_{args.alg}_merkle_inplace_hash_throughput".replace("-", ""),
+        "value": round(value, 4), "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 3),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "sample": sample},
-        "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": cores, "kind": "port", "sample": sample,
-                         "c_port_all_threads_gbs": round(c_gbs, 3)},
+        "config": {"workload": WORKLOAD if headline else f"{args.arch} {args.alg} Merkle in-place hash, block {BLOCK}",
+                   "bytes": total_bytes, "leaves": n_leaves, "tensors": len(host),
+                   "root": root, "root_matches_pinned": root_ok, "sample": sample, "sample_bytes": sample_bytes},
+        "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": cores, "kind": kind, "sample": sample},
         "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }
     print(json.dumps(line), flush=True)
 
 
-# ----------------------------------------------------------------------------- GPU side
+# ----------------------------------------------------------------------------- GPU side helpers
+
+def cuda_time_ms(fn, steps, warmup=2):
+    import torch
+
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / steps
+
+
+def run_intpeak():
+    exe = ROOT / "tools" / "_build" / "intpeak"
+    if not exe.exists():
+        return None
+    try:
+        out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120).stdout
+        return json.loads(out.strip().splitlines()[-1])
+    except Exception as exc:                   # the microbenchmark is evidence, not a dependency
+        return {"error": str(exc)}
+
+
+def model_roofline(alg, arch, kernel_ms, leaves, nbytes, step_ms, hbm_peak, peak_src, peaks, traffic):
+    """Roofline of the leaf-stage launch (the dominant kernel): HBM fraction per contract, and the unit that binds."""
+    achieved = nbytes / (kernel_ms * 1e-3) / 1e9
+    r = {"bound": "hbm", "kernel": f"merkle_fused_kernel<{alg}> (persistent leaf stage)", "achieved": round(achieved, 1),
+         "peak": hbm_peak, "unit": "GB/s", "frac": round(achieved / hbm_peak, 4), "traffic": traffic,
+         "peak_source": peak_src, "kernel_ms": round(kernel_ms, 4), "share_of_step": round(kernel_ms / step_ms, 4),
+         "algorithmic_bytes": nbytes}
+    if peaks and "error" not in peaks:
+        alu_peak = max(peaks["lop3_tops"], peaks["shf_tops"], peaks["iadd3_tops"])
+        fma_peak = peaks.get("imad_tops", alu_peak)
+        alu = ALU_PER_LEAF[alg] * leaves / (kernel_ms * 1e-3) / 1e12
+        fma = FMA_PER_LEAF[alg] * leaves / (kernel_ms * 1e-3) / 1e12
+        r.update({"binding_unit": "integer ALU pipe (SHF / LOP3 / PRMT / IADD3, 64 lanes/clk/SM)",
+                  "binding_unit_frac": round(alu / alu_peak, 4),
+                  "alu_pipe_tops": round(alu, 3), "alu_peak_tops": round(alu_peak, 3),
+                  "fma_pipe_tops": round(fma, 3), "fma_peak_tops": round(fma_peak, 3),
+                  "issue_budget_frac": round((alu + fma) / (alu_peak + fma_peak), 4),
+                  "note": "binding roofline is the integer ALU pipe; the HBM fraction is reported per contract. "
+                          "Instruction counts per leaf from profiles/r2_sass_report.txt, peaks from tools/intpeak."})
+    return r
+
+
+def gpu_model_config(pkg, dev, shapes, arch, alg, device, steps, hbm_peak, peak_src, peaks, ref, cores, traffic_db):
+    """One ride-along Merkle configuration: GPU time, roofline, and the reference on the same bytes (root asserted)."""
+    import torch
+
+    sd = shapes.synthetic_state_dict(arch, device, seed=0)
+    plan = dev.ModelPlan([dev.as_device_bytes(t) for _, t in sd], BLOCK)
+    hasher = dev.MerkleModelHasher(plan, alg)
+    step_ms = cuda_time_ms(hasher.run, steps, 3)
+    leaf_ms = cuda_time_ms(hasher.run_leaves_only, steps, 2)
+    hasher.run()
+    root = hasher.out_bytes().hex()
+    out = {"workload": f"{arch} (random-init fp32) {alg} Merkle in-place hash, block {BLOCK}", "arch": arch, "alg": alg,
+           "bytes": plan.total_bytes, "leaves": plan.leaf_count, "tensors": len(sd),
+           "ms_per_step": round(step_ms, 4), "value": round(plan.total_bytes / step_ms / 1e6, 2), "unit": UNIT,
+           "root": root,
+           "roofline": model_roofline(alg, arch, leaf_ms, plan.leaf_count, plan.total_bytes, step_ms, hbm_peak, peak_src,
+                                      peaks, traffic_db.get(f"merkle_fused_kernel<{alg}>:{arch}"))}
+    if ref is not None:
+        host = host_views(sd)
+        cfg = reference_cfg(ref, alg)
+        dt_all, res = timed_cpu(lambda: ref.hash_model(cfg, reference_model(ref, host), workers=cores))
+        assert res.model_digest.data.hex() == root, f"{arch}/{alg}: GPU root differs from the reference package's"
+        leaves_ref, n_ref, n_tensors = reference_leaf_digests(ref, alg, host, 64 << 20)
+        dl = dev.DIGEST_LEN[alg]
+        assert hasher.leaf_bytes()[:n_ref * dl] == leaves_ref, f"{arch}/{alg}: leaf digests differ from the reference's"
+        out["cpu_baseline"] = {"value": round(plan.total_bytes / dt_all / 1e9, 4), "unit": UNIT, "cores": cores,
+                               "kind": "reference", "ms": round(dt_all * 1e3, 1),
+                               "sample": f"sentinel.hash_model(workers={cores}) over the D2H copy of the full state dict, one pass",
+                               "parity": f"root identical; first {n_ref} leaf digests ({n_tensors} tensors) identical"}
+    del hasher
+    plan.close()
+    del plan, sd
+    torch.cuda.empty_cache()
+    return out
+
+
+def cifar_shaped(np):
+    n, ln, n_src = 50_000, 3072, 16
+    data = np.random.default_rng(0).integers(0, 256, size=n * ln, dtype=np.uint8)
+    r1 = np.random.default_rng(1)
+    src = r1.choice(n_src, size=n, p=r1.dirichlet(np.ones(n_src)))
+    offs = np.arange(n, dtype=np.uint64) * ln
+    return data, offs, np.full(n, ln, dtype=np.uint64), np.arange(n, dtype=np.uint64), src, n_src
+
+
+def hellaswag_shaped(np):
+    n, n_cur, vocab = 40_000, 16, 50257
+    lens_tok = np.clip(np.rint(np.random.default_rng(2).lognormal(np.log(90.0), 0.4, n)), 16, 256).astype(np.int64)
+    lengths = (lens_tok * 4).astype(np.uint64)
+    offsets = np.zeros(n, dtype=np.uint64)
+    np.cumsum(lengths[:-1], out=offsets[1:])
+    tokens = np.random.default_rng(2).integers(0, vocab, size=int(lens_tok.sum()), dtype=np.int32)
+    r3 = np.random.default_rng(3)
+    curator = r3.choice(n_cur, size=n, p=r3.dirichlet(np.ones(n_cur)))
+    return tokens.view(np.uint8), offsets, lengths, np.arange(n, dtype=np.uint64), curator, n_cur
+
+
+def reference_dataset_digests(ref, shard, offs, lens, ids, src, n_src, batch=128):
+    """The reference's loader loop: SourceAccumulator + process_batch over batches of 128, then finalize."""
+    view = memoryview(shard)
+    acc = ref.SourceAccumulator()
+    acc.declare(range(n_src))
+    n = len(ids)
+    t0 = time.perf_counter()
+    for s in range(0, n, batch):
+        recs = [ref.SampleRecord(int(ids[i]), int(src[i]), b"", bytes(view[int(offs[i]):int(offs[i] + lens[i])]))
+                for i in range(s, min(n, s + batch))]
+        ref.process_batch(ref.Batch(recs), acc)
+    out = ref.finalize(acc)
+    return time.perf_counter() - t0, out
+
+
+def dataset_config(name, workload, arrays, np, torch, dsm, dev, dd, world, rank, steps, warmup, barrier, device,
+                   hbm_peak, peak_src, peaks, ref, cores):
+    """A LtHash dataset configuration: device-resident samples/s, end to end from pinned host memory, the
+    reference loop on the same samples (per-source digests and counts asserted), roofline of the kernel."""
+    import torch.distributed as dist
+
+    shard, offs, lens, ids, src, n_src = arrays
+    n = len(ids)
+    shard_h = torch.from_numpy(shard).pin_memory()
+    dset = dsm.DeviceDataset.from_host(shard_h, offs, lens, ids, src, list(range(n_src)))
+    a, b = dd.sample_ranges(n, world)[rank]
+    acc = dev.LatticeAccumulator(n_src)
+
+    def ds_step():
+        acc.zero_()
+        dset.accumulate(acc, a, b)
+        if world > 1:
+            dd.allreduce_lattice(acc.state)
+
+    for _ in range(max(warmup, 3)):
+        ds_step()
+    barrier()
+    d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    d0.record()
+    for _ in range(steps):
+        ds_step()
+    d1.record()
+    barrier()
+    ds_ms = d0.elapsed_time(d1) / steps
+    kernel_ms = cuda_time_ms(lambda: dset.accumulate(acc, a, b), steps, 2)
+    if world > 1:
+        t = torch.tensor([ds_ms], device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ds_ms = float(t.item())
+    ds_step()
+    digests, counts, status = acc.digests()
+    assert status == 0
+    lo = int(offs[a])
+    hi = int(offs[b - 1] + lens[b - 1]) if b > a else lo
+
+    def ds_e2e():       # rows and shard bytes of this rank's range from pinned host memory each step, digests back
+        d = dsm.DeviceDataset.from_host(shard_h[lo:hi], offs[a:b] - np.uint64(lo), lens[a:b], ids[a:b], src[a:b],
+                                        list(range(n_src)))
+        acc2 = dev.LatticeAccumulator(n_src)
+        d.accumulate(acc2)
+        if world > 1:
+            dd.allreduce_lattice(acc2.state)
+        return acc2.digests()
+
+    ds_e2e()
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(5):
+        ds_e2e()
+    barrier()
+    ds_dt = (time.perf_counter() - t0) / 5
+    nbytes = int(lens.sum())
+    my_bytes = int(lens[a:b].sum())
+    blocks = int(((lens[a:b] + np.uint64(8 + 127)) // np.uint64(128)).sum())
+    achieved = my_bytes / (kernel_ms * 1e-3) / 1e9
+    roof = {"bound": "hbm", "kernel": "lthash kernel (BLAKE2b per sample + per-source lane sums)", "achieved": round(achieved, 1),
+            "peak": hbm_peak, "unit": "GB/s", "frac": round(achieved / hbm_peak, 4), "traffic": None, "peak_source": peak_src,
+            "kernel_ms": round(kernel_ms, 4), "share_of_step": round(kernel_ms / ds_ms, 4), "algorithmic_bytes": my_bytes}
+    if peaks and "error" not in peaks:
+        alu_peak = max(peaks["lop3_tops"], peaks["shf_tops"], peaks["iadd3_tops"])
+        alu = LT_ALU_PER_BLOCK * blocks / (kernel_ms * 1e-3) / 1e12
+        roof.update({"binding_unit": "integer ALU pipe", "binding_unit_frac": round(alu / alu_peak, 4),
+                     "alu_pipe_tops": round(alu, 3), "alu_peak_tops": round(alu_peak, 3), "blake2b_blocks": blocks})
+    out = {"metric": f"{name}_lthash_samples_per_s", "workload": workload, "value": round(n / (ds_ms * 1e-3), 1),
+           "unit": "samples/s", "ms_per_step": round(ds_ms, 4), "samples": n, "sources": n_src, "bytes": nbytes,
+           "gbs": round(nbytes / (ds_ms * 1e-3) / 1e9, 2), "roofline": roof,
+           "e2e": {"value": round(n / ds_dt, 1), "unit": "samples/s", "ms_per_step": round(ds_dt * 1e3, 3),
+                   "h2d_bytes_per_step": int(hi - lo) + 28 * (b - a), "d2h_bytes_per_step": n_src * 72 + 8}}
+    if world == 1:
+        # the reference-shaped loader loop on this engine: process_batch over batches of 128 host records
+        def api_loop():
+            view = memoryview(shard)
+            sacc = dsm.SourceAccumulator()
+            sacc.declare(range(n_src))
+            for s in range(0, n, 128):
+                recs = [dsm.SampleRecord(int(ids[i]), int(src[i]), b"", bytes(view[int(offs[i]):int(offs[i] + lens[i])]))
+                        for i in range(s, min(n, s + 128))]
+                dsm.process_batch(dsm.Batch(recs), sacc)
+            return dsm.finalize(sacc)
+
+        api_loop()
+        dt_api, got_api = timed_cpu(api_loop, 2)
+        for i in range(n_src):
+            assert (got_api[i][0].data, got_api[i][1]) == (digests[64 * i:64 * i + 64], counts[i]), \
+                f"{name}: process_batch loop differs from the one-launch digest for source {i}"
+        out["process_batch_api"] = {"value": round(n / dt_api, 1), "unit": "samples/s", "ms": round(dt_api * 1e3, 1),
+                                    "api": "SourceAccumulator + process_batch(Batch of 128 host SampleRecords) x "
+                                           f"{-(-n // 128)} + finalize, host wall clock incl. building the records"}
+    if ref is not None and world == 1:
+        dt, want = reference_dataset_digests(ref, shard, offs, lens, ids, src, n_src)
+        for i in range(n_src):
+            assert (digests[64 * i:64 * i + 64], counts[i]) == (want[i][0].data, want[i][1]), \
+                f"{name}: source {i} differs from the reference package's digest"
+        out["cpu_baseline"] = {"value": round(n / dt, 1), "unit": "samples/s", "cores": 1, "kind": "reference",
+                               "ms": round(dt * 1e3, 1),
+                               "sample": "sentinel.SourceAccumulator + process_batch over all samples in batches of 128, "
+                                         "finalize (single thread, as the reference runs it)",
+                               "parity": f"all {n_src} per-source digests and counts identical"}
+    return out, (digests, counts)
+
+
+# ----------------------------------------------------------------------------- GPU arm
 
 def run_ours(args):
     import numpy as np
@@ -198,7 +512,8 @@ def run_ours(args):
     import torch.distributed as dist
 
     import paper_2510_00554_b200 as pkg
-    from paper_2510_00554_b200 import _native, dataset as dsm, device as dev, distributed as dd, shapes
+    from paper_2510_00554_b200 import _native, attestation as att, dataset as dsm, device as dev, distributed as dd, shapes
+    from paper_2510_00554_b200.model import INDEX_ENCODING
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -218,11 +533,21 @@ def run_ours(args):
     lib = _native.load()
     device = torch.device("cuda", local_rank)
     hbm_peak, peak_src = measured_peaks()
+    cores = os.cpu_count() or 1
+    ref = load_reference() if (rank == 0 and world == 1 and not args.no_cpu_baseline) else None
+    traffic_db = {}
+    prof = ROOT / "profiles" / "ncu_traffic.json"
+    if prof.exists():
+        try:
+            traffic_db = json.loads(prof.read_text())
+        except Exception:
+            traffic_db = {}
 
     # ---- workload: random-init fp32 state dict, every tensor its own allocation
     sd = shapes.synthetic_state_dict(args.arch, device, seed=0)
+    n_tensors = len(sd)
     flat = [dev.as_device_bytes(t) for _, t in sd]
-    plan = dev.ModelPlan(flat, 8192)
+    plan = dev.ModelPlan(flat, BLOCK)
     total_bytes, n_leaves = plan.total_bytes, plan.leaf_count
     sp = dd.plan_shards(n_leaves, world)
     backend = dd.CudaBackend(plan, args.alg)
@@ -265,115 +590,97 @@ def run_ours(args):
     ms_step = ms_total / args.steps
     value = total_bytes / (ms_step * 1e-3) / 1e9
 
-    # ---- dominant kernel (leaf hashing) alone, CUDA events on the launching stream
+    # ---- dominant kernel (the persistent leaf-stage launch) alone, CUDA events on the launching stream
     begin, end = sp.leaf_range(rank)
     leaf_hasher = whole if world == 1 else dev.MerkleModelHasher(plan, args.alg, begin, end, sp.levels)
-    for _ in range(2):
-        leaf_hasher.run_leaves_only()
-    torch.cuda.synchronize()
-    k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    k0.record()
-    for _ in range(args.steps):
-        leaf_hasher.run_leaves_only()
-    k1.record()
-    torch.cuda.synchronize()
-    leaf_ms = k0.elapsed_time(k1) / args.steps
+    leaf_ms = cuda_time_ms(leaf_hasher.run_leaves_only, args.steps, 2)
     my_leaves = end - begin
-    my_bytes = total_bytes * my_leaves / n_leaves
-    achieved = my_bytes / (leaf_ms * 1e-3) / 1e9
-    roofline = {"bound": "hbm", "kernel": f"merkle_leaf_kernel<{args.alg}>", "achieved": round(achieved, 1),
-                "peak": hbm_peak, "unit": "GB/s", "frac": round(achieved / hbm_peak, 4), "traffic": None,
-                "peak_source": peak_src, "kernel_ms": round(leaf_ms, 4),
-                "share_of_step": round(leaf_ms / ms_step, 4),
-                "note": "binding roofline is the integer ALU pipe (see int_pipe); HBM fraction reported per contract"}
-    prof = ROOT / "profiles" / "ncu_traffic.json"
-    if prof.exists():
-        try:
-            whole = json.loads(prof.read_text()).get(f"merkle_leaf_kernel<{args.alg}>:{args.arch}")
-            # per launch, like `achieved`: a rank's launch covers its share of the leaves
-            roofline["traffic"] = whole if (whole is None or world == 1) else int(whole * my_leaves / n_leaves)
-        except Exception:
-            pass
-
-    # ---- integer-pipe roofline: measured on this box by tools/intpeak
+    my_bytes = int(total_bytes * my_leaves / n_leaves)
+    peaks = run_intpeak() if (rank == 0 and not args.no_intpeak) else None
+    traffic = traffic_db.get(f"merkle_fused_kernel<{args.alg}>:{args.arch}")
+    if traffic is not None and world > 1:
+        traffic = int(traffic * my_leaves / n_leaves)      # per launch, like `achieved`
+    roofline = model_roofline(args.alg, args.arch, leaf_ms, my_leaves, my_bytes, ms_step, hbm_peak, peak_src, peaks, traffic)
     int_pipe = None
-    intpeak_bin = ROOT / "tools" / "_build" / "intpeak"
-    if rank == 0 and intpeak_bin.exists() and args.alg == "sha256" and not args.no_intpeak:
-        try:
-            out = subprocess.run([str(intpeak_bin)], capture_output=True, text=True, timeout=120).stdout
-            peaks = json.loads(out.strip().splitlines()[-1])
-            alu_peak = max(peaks["lop3_tops"], peaks["shf_tops"], peaks["iadd3_tops"])
-            ops = SHA256_OPS_PER_LEAF * my_leaves / (leaf_ms * 1e-3) / 1e12
-            alu_ops = SHA256_ALU_INSTR_PER_LEAF * my_leaves / (leaf_ms * 1e-3) / 1e12
-            ceiling = peaks.get("sha256_fma_regs_gbs") or peaks["sha256_regs_gbs"]
-            int_pipe = {"achieved_tops": round(ops, 3), "alu_peak_tops": round(alu_peak, 3),
-                        "frac_of_alu_peak": round(ops / alu_peak, 4),
-                        "alu_pipe_tops": round(alu_ops, 3), "alu_pipe_utilisation": round(alu_ops / alu_peak, 4),
-                        "compute_only_gbs": ceiling, "compute_only_stock_gbs": peaks.get("sha256_regs_gbs"),
-                        "frac_of_compute_only": round(achieved / ceiling, 4),
-                        "ops_model": "180,600 32-bit ops per 8 KiB leaf (SURVEY.md 8(d)); the kernel issues "
-                                     f"{SHA256_ALU_INSTR_PER_LEAF:,} of them on the ALU pipe and the additions as "
-                                     "IMAD on the FMA pipe, so achieved_tops may exceed the ALU-only peak",
-                        "microbench": peaks}
-            # the unit that actually binds this kernel, next to the contractual HBM fraction
-            roofline["binding_unit"] = "integer ALU pipe (SHF/LOP3/PRMT at 64 lanes/clk/SM)"
-            roofline["binding_unit_frac"] = int_pipe["alu_pipe_utilisation"]
-        except Exception as exc:       # the microbenchmark is evidence, not a dependency
-            int_pipe = {"error": str(exc)}
+    if peaks and "error" not in peaks and args.alg == "sha256":
+        ceiling = peaks.get("sha256_fma_regs_gbs") or peaks.get("sha256_regs_gbs")
+        int_pipe = {"alu_pipe_utilisation": roofline.get("binding_unit_frac"),
+                    "issue_budget_frac": roofline.get("issue_budget_frac"),
+                    "model_ops_tops": round(SHA256_OPS_PER_LEAF * my_leaves / (leaf_ms * 1e-3) / 1e12, 3),
+                    "compute_only_gbs": ceiling,
+                    "frac_of_compute_only": round(roofline["achieved"] / ceiling, 4) if ceiling else None,
+                    "ops_model": "model_ops_tops counts SURVEY.md 8(d)'s 180,600 abstract 32-bit ops per leaf; the kernel "
+                                 "issues them as ALU-pipe and FMA-pipe (IMAD) instructions, so utilisation is stated per "
+                                 "pipe and against the combined issue budget, never above 1",
+                    "microbench": peaks}
+    elif peaks:
+        int_pipe = {"microbench": peaks}
+
+    # ---- the three schedules of the same hash, for the record (one GPU)
+    schedules = None
+    if world == 1:
+        schedules = {}
+        for name, sched in (("fused_single_launch", _native.SCHEDULE_FUSED), ("grid_round1", _native.SCHEDULE_GRID)):
+            lib.snt_merkle_schedule(sched)
+            l0 = int(lib.snt_debug_launch_count())
+            whole.run()
+            per_hash = int(lib.snt_debug_launch_count()) - l0
+            ms = cuda_time_ms(whole.run, max(5, args.steps // 2), 2)
+            assert whole.out_bytes().hex() == root_hex
+            schedules[name] = {"ms_per_step": round(ms, 4), "launches_per_hash": per_hash}
+        lib.snt_merkle_schedule(_native.SCHEDULE_PERSISTENT)
+        schedules["persistent_default"] = {"ms_per_step": round(ms_step, 4), "launches_per_hash": launches // args.steps}
 
     # ---- the public call on tensors that already live in HBM: hash_model(cfg, TensorMap(cuda tensors)),
-    #      host wall clock per call (plan build + 3 launches + 32-byte readback); explains value vs e2e
+    #      host wall clock per call (cached plan + workspace, launches, 32-byte readback)
     api_resident = None
+    cfg = pkg.HashConfig(pkg.Construction.MERKLE, pkg.Strategy.IN_PLACE, pkg.CompressionAlg.from_name(args.alg))
     if world == 1:
-        cfg_r = pkg.HashConfig(pkg.Construction.MERKLE, pkg.Strategy.IN_PLACE, pkg.CompressionAlg.from_name(args.alg))
         model_r = pkg.TensorMap([(name, t) for name, t in sd])
         for _ in range(2):
-            got_r = pkg.hash_model(cfg_r, model_r).model_digest.data
+            got_r = pkg.hash_model(cfg, model_r).model_digest.data
         assert got_r.hex() == root_hex, "hash_model on resident tensors differs from the planned hasher"
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         for _ in range(args.steps):
-            pkg.hash_model(cfg_r, model_r)
+            pkg.hash_model(cfg, model_r)
         dt_r = (time.perf_counter() - t0) / args.steps
         api_resident = {"value": round(total_bytes / dt_r / 1e9, 2), "unit": UNIT, "ms_per_call": round(dt_r * 1e3, 4),
+                        "overhead_vs_value_pct": round((dt_r * 1e3 / ms_step - 1) * 100, 2),
                         "api": "hash_model(cfg, TensorMap(CUDA tensors)), host wall clock"}
         del model_r
 
     # ---- end to end through the public API: pinned host tensors -> hash_model -> root bytes
     e2e = None
+    host_pinned = {}
     if not args.no_e2e:
-        cfg = pkg.HashConfig(pkg.Construction.MERKLE, pkg.Strategy.IN_PLACE, pkg.CompressionAlg.from_name(args.alg))
         host_entries = []
-        seen = {}
         first_leaf = 0
         my_a, my_b = sp.leaf_range(rank)
         for name, t in sd:
             nbytes = t.numel() * 4
-            next_leaf = first_leaf + -(-nbytes // 8192)
+            next_leaf = first_leaf + -(-nbytes // BLOCK)
             mine = world == 1 or (first_leaf < my_b and next_leaf > my_a)
             key = (t.data_ptr(), mine)
-            if key not in seen:
+            if key not in host_pinned:
                 if mine:
                     h = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
                     h.copy_(t.reshape(-1).view(torch.uint8))
                 else:
                     h = torch.empty(nbytes, dtype=torch.uint8)   # never read by this rank: not pinned, not touched
-                seen[key] = h
-            host_entries.append((name, seen[key]))
+                host_pinned[key] = h
+            host_entries.append((name, host_pinned[key]))
             first_leaf = next_leaf
         torch.cuda.synchronize()
+        model = pkg.TensorMap(host_entries)
         if world == 1:
-            model = pkg.TensorMap(host_entries)
-
             def e2e_step():
                 return pkg.hash_model(cfg, model).model_digest.data
             h2d = total_bytes
         else:
-            model = pkg.TensorMap(host_entries)
-
             def e2e_step():
                 return dd.hash_model_sharded(cfg, model, rank, world).model_digest.data
-            h2d = dd.staged_bytes(model, 8192, *sp.leaf_range(rank))
+            h2d = dd.staged_bytes(model, BLOCK, *sp.leaf_range(rank))
         got = e2e_step()
         assert got.hex() == root_hex, "e2e digest differs from the device-resident digest"
         barrier()
@@ -389,80 +696,101 @@ def run_ours(args):
         e2e = {"value": round(total_bytes / dt / 1e9, 3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": 32, "ms_per_step": round(dt * 1e3, 3), "steps": args.e2e_steps,
                "api": "hash_model(HashConfig(MERKLE, IN_PLACE, SHA256, 8192), TensorMap(pinned host tensors))"}
-        del host_entries, seen, model
+        del model, host_entries
 
-    # ---- CIFAR10-shaped LtHash dataset (BASELINE config 3), samples/s
-    dataset = None
-    if not args.no_dataset:
-        n, ln, n_src = 50_000, 3072, 16
-        rng = np.random.default_rng(0)
-        shard_h = torch.from_numpy(rng.integers(0, 256, size=n * ln, dtype=np.uint8)).pin_memory()
-        src = np.random.default_rng(1).choice(n_src, size=n, p=np.random.default_rng(1).dirichlet(np.ones(n_src)))
-        offs = np.arange(n, dtype=np.uint64) * ln
-        lens = np.full(n, ln, dtype=np.uint64)
-        ids = np.arange(n, dtype=np.uint64)
-        dset = dsm.DeviceDataset.from_host(shard_h, offs, lens, ids, src, list(range(n_src)))
-        a, b = dd.sample_ranges(n, world)[rank]
-        acc = dev.LatticeAccumulator(n_src)
-
-        def ds_step():
-            acc.zero_()
-            dset.accumulate(acc, a, b)
-            if world > 1:
-                dd.allreduce_lattice(acc.acc, acc.counts)
-
-        for _ in range(args.warmup):
-            ds_step()
-        barrier()
-        d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        d0.record()
-        for _ in range(args.steps):
-            ds_step()
-        d1.record()
-        barrier()
-        ds_ms = d0.elapsed_time(d1) / args.steps
-        if world > 1:
-            t = torch.tensor([ds_ms], device=device)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ds_ms = float(t.item())
-        # e2e: shard rows from pinned host memory each step, digests back to the host
-        def ds_e2e():
-            d = dsm.DeviceDataset.from_host(shard_h[a * ln:b * ln], offs[:b - a], lens[a:b], ids[a:b], src[a:b],
-                                            list(range(n_src)))
-            acc2 = dev.LatticeAccumulator(n_src)
-            d.accumulate(acc2)
-            if world > 1:
-                dd.allreduce_lattice(acc2.acc, acc2.counts)
-            return acc2.digests()
-        ds_e2e()
-        barrier()
-        t0 = time.perf_counter()
-        for _ in range(5):
-            ds_e2e()
-        barrier()
-        ds_dt = (time.perf_counter() - t0) / 5
-        dataset = {"metric": "cifar10_shaped_lthash_samples_per_s", "value": round(n / (ds_ms * 1e-3), 1),
-
-                   "unit": "samples/s", "ms_per_step": round(ds_ms, 4), "samples": n, "bytes": n * ln,
-                   "gbs": round(n * ln / (ds_ms * 1e-3) / 1e9, 2),
-                   "e2e": {"value": round(n / ds_dt, 1), "unit": "samples/s", "ms_per_step": round(ds_dt * 1e3, 3),
-                           "h2d_bytes_per_step": int((b - a) * (ln + 28)), "d2h_bytes_per_step": n_src * 72}}
-
-    # ---- CPU baseline on this box's host cores (rank 0, N=1 only), bounded sample
+    # ---- CPU baseline on this box's host cores (rank 0, N = 1): the reference package on the SAME bytes,
+    #      bit-exactness asserted before anything is printed
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cores = os.cpu_count() or 1
-        tensors, total = host_model_sample(args.arch, args.cpu_sample_mb << 20)
-        c_gbs, c_dt = cpu_baseline_c(args.alg, tensors, total, cores)
-        py_tensors, py_total = host_model_sample(args.arch, min(args.cpu_sample_mb, 512) << 20)
-        py_gbs, py_dt = cpu_baseline_python(args.alg, py_tensors, py_total, cores)
-        py1_gbs, _ = cpu_baseline_python(args.alg, py_tensors[:1], py_tensors[0].size, 1)
-        cpu = {"value": round(py_gbs, 4), "unit": UNIT, "cores": cores, "kind": "port",
-               "sample": (f"Python/hashlib port of the reference with a {cores}-thread pool over the first "
-                          f"{len(py_tensors)} tensors ({py_total / 1e6:.0f} MB) of the same state-dict layout"),
-               "single_thread_gbs": round(py1_gbs, 4),
-               "c_port": {"value": round(c_gbs, 3), "unit": UNIT, "threads": cores, "sample_mb": round(total / 1e6),
-                          "note": "plain-C oracle, pthreads over contiguous leaf ranges, SHA-NI if the CPU has it"}}
+    if ref is not None:
+        if host_pinned:                       # the pinned copies made for e2e ARE the D2H copy of the GPU tensors
+            host = [(name, host_pinned[(t.data_ptr(), True)].numpy()) for name, t in sd]
+        else:
+            host = host_views(sd)
+        rcfg = reference_cfg(ref, args.alg)
+        dt_all, res = timed_cpu(lambda: ref.hash_model(rcfg, reference_model(ref, host), workers=cores))
+        assert res.model_digest.data.hex() == root_hex, "GPU root differs from the reference package's root"
+        assert res.block_count == n_leaves
+        leaves_ref, n_ref, n_ref_tensors = reference_leaf_digests(ref, args.alg, host, 256 << 20)
+        dl = dev.DIGEST_LEN[args.alg]
+        whole.run()
+        assert whole.leaf_bytes()[:n_ref * dl] == leaves_ref, "GPU leaf digests differ from the reference package's"
+        # workers = 1 and the sequential (Sigstore/hashlib-style) baseline on a bounded prefix of the same bytes
+        prefix, pbytes = [], 0
+        for name, arr in host:
+            if prefix and pbytes + arr.size > (1 << 30):
+                break
+            prefix.append((name, arr))
+            pbytes += arr.size
+        dt_1, _ = timed_cpu(lambda: ref.hash_model(rcfg, reference_model(ref, prefix), workers=1))
+        dt_seq, _ = timed_cpu(lambda: ref.sequential_hash(ref.CompressionAlg.from_name(args.alg),
+                                                          iter([memoryview(a) for _, a in prefix])))
+        cpu = {"value": round(total_bytes / dt_all / 1e9, 4), "unit": UNIT, "cores": cores, "kind": "reference",
+               "ms": round(dt_all * 1e3, 1),
+               "sample": f"sentinel.hash_model(MERKLE, IN_PLACE, {args.alg}, 8192, workers={cores}) over the D2H copy of "
+                         f"the full state dict ({total_bytes / 1e9:.2f} GB), one pass",
+               "parity": f"root identical; first {n_ref} leaf digests ({n_ref_tensors} tensors) identical; block_count identical",
+               "workers_1_gbs": round(pbytes / dt_1 / 1e9, 4),
+               "sequential_hash_gbs": round(pbytes / dt_seq / 1e9, 4),
+               "prefix_sample": f"workers=1 and sequential_hash: the first {len(prefix)} tensors ({pbytes / 1e6:.0f} MB)"}
+        try:                                   # context: what compiled host code does on the same cores
+            from oracle import c_oracle
+
+            tl = c_oracle.TensorList([a for _, a in prefix])
+            dt_c, _ = timed_cpu(lambda: c_oracle.inplace_merkle(args.alg, tl, BLOCK, cores), 2)
+            cpu["c_port_all_threads_gbs"] = round(pbytes / dt_c / 1e9, 3)
+        except Exception:
+            pass
+        del host, prefix
+    host_pinned.clear()
+
+    # ---- the other BASELINE configurations
+    configs = None
+    if not args.no_configs:
+        configs = []
+        if world == 1:
+            del whole, leaf_hasher, backend
+            plan.close()
+            del plan, flat, sd
+            torch.cuda.empty_cache()
+            for arch, alg in (("gpt2", "sha256"), ("bert-large", "blake2b"), ("bert-large", "sha3-256"),
+                              ("vgg19", "blake2b"), ("vgg19", "sha3-256")):
+                configs.append(gpu_model_config(pkg, dev, shapes, arch, alg, device, args.steps, hbm_peak, peak_src, peaks,
+                                                ref, cores, traffic_db))
+        cifar, _ = dataset_config("cifar10_shaped", "CIFAR10-shaped synthetic dataset (50,000 x 3,072 B uint8, 16 sources) LtHash",
+                                  cifar_shaped(np), np, torch, dsm, dev, dd, world, rank, args.steps, args.warmup, barrier,
+                                  device, hbm_peak, peak_src, peaks, ref, cores)
+        configs.append(cifar)
+        pool_arrays = hellaswag_shaped(np)
+        pool, (pdig, pcounts) = dataset_config(
+            "hellaswag_shaped_pool", "hellaswag-shaped token arrays (40,000 ragged samples, 16 curators) LtHash", pool_arrays,
+            np, torch, dsm, dev, dd, world, rank, args.steps, args.warmup, barrier, device, hbm_peak, peak_src, peaks, ref, cores)
+        if rank == 0:
+            # config 5 end to end: one signed bundle per curator + one for the GPT2-XL root, then verification
+            n_cur = pool_arrays[5]
+            keys = [att.KeyPair.generate() for _ in range(n_cur + 1)]
+            t0 = time.perf_counter()
+            bundles = []
+            for c in range(n_cur):
+                stmt = att.Statement([att.Subject(f"pool.json:source:{c}", {"lthash": pdig[64 * c:64 * c + 64].hex()})],
+                                     att.DATASET_PREDICATE_TYPE,
+                                     {"source_id": c, "sample_count": pcounts[c], "cover_labels": False,
+                                      "index_encoding": INDEX_ENCODING})
+                bundles.append(att.sign_bundle(stmt, keys[c]))
+            bundles.append(att.sign_bundle(att.Statement([att.Subject("gpt2-xl", {"sha256": root_hex})],
+                                                         att.MODEL_PREDICATE_TYPE, cfg.predicate()), keys[n_cur]))
+            t_sign = time.perf_counter() - t0
+            t0 = time.perf_counter()
+            verdicts = [att.verify_bundle(bundles[c], {f"pool.json:source:{c}": {"lthash": pdig[64 * c:64 * c + 64].hex()}})
+                        for c in range(n_cur)]
+            verdicts.append(att.verify_bundle(bundles[n_cur], {"gpt2-xl": {"sha256": root_hex}}))
+            t_verify = time.perf_counter() - t0
+            assert all(v is att.Verdict.OK for v in verdicts)
+            pool["sign_verify"] = {"bundles": n_cur + 1, "ecdsa_sign_ms": round(t_sign * 1e3, 3),
+                                   "ecdsa_verify_ms": round(t_verify * 1e3, 3), "all_verified": True,
+                                   "model_hash_ms": round(ms_step, 4),
+                                   "end_to_end_ms": round(pool["e2e"]["ms_per_step"] + ms_step + (t_sign + t_verify) * 1e3, 3),
+                                   "note": "dataset e2e (H2D + LtHash + D2H) + GPT2-XL Merkle root (resident) + host ECDSA P-256"}
+        configs.append(pool)
 
     if rank == 0:
         line = {
@@ -472,25 +800,59 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
             "config": {"workload": WORKLOAD if args.arch == "gpt2-xl" and args.alg == "sha256"
-                       else f"{args.arch} {args.alg} Merkle in-place hash, block 8192",
-                       "bytes": total_bytes, "leaves": n_leaves, "tensors": len(sd),
+                       else f"{args.arch} {args.alg} Merkle in-place hash, block {BLOCK}",
+                       "bytes": total_bytes, "leaves": n_leaves, "tensors": n_tensors,
                        "parallelism": f"leaf-range sharding x{world}, shard = 2^{sp.levels} leaves",
                        "l2_policy": "inputs (6.55 GB per pass) larger than the 126 MB L2",
-                       "root": root_hex},
+                       "root": root_hex, "root_matches_pinned": PINNED_ROOTS.get((args.arch, args.alg), root_hex) == root_hex},
             **({"debug": "ranks share GPU 0 over gloo; not a measurement"} if same_gpu else {}),
-            "e2e": e2e, "api_device_resident": api_resident, "gpu_launches": launches, "clocks": clocks.summary(), "roofline": roofline,
-            "int_pipe": int_pipe, "cpu_baseline": cpu, "dataset": dataset,
+            "e2e": e2e, "api_device_resident": api_resident, "gpu_launches": launches, "clocks": clocks.summary(),
+            "roofline": roofline, "int_pipe": int_pipe, "cpu_baseline": cpu, "schedules": schedules, "configs": configs,
+            # kept for readers of round 1's line: the CIFAR10-shaped entry of `configs`
+            "dataset": next((c for c in (configs or []) if c.get("metric", "").startswith("cifar10")), None),
         }
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
 
 
+# ----------------------------------------------------------------------------- launch
+
+def free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def self_launch(args) -> int:
+    """`--gpus N` outside torchrun: start N ranks of this script, one per GPU, over NCCL."""
+    import torch
+
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        print(json.dumps({"metric": METRIC, "n_gpus": args.gpus, "unavailable":
+                          f"--gpus {args.gpus} needs {args.gpus} CUDA devices, this box has {have}"}), flush=True)
+        print(f"bench.py: --gpus {args.gpus} needs {args.gpus} CUDA devices, this box has {have}", file=sys.stderr)
+        return 2
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")           # communicator / rank lines on stderr
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    env.setdefault("OMP_NUM_THREADS", "4")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()), str(Path(__file__).resolve()), *sys.argv[1:]]
+    return subprocess.call(cmd, env=env)
+
+
 def main():
     args = parse_args()
     if args.impl == "reference":
         run_reference(args)
+    elif args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args))
     else:
+        if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         run_ours(args)
 
 

@@ -46,7 +46,7 @@ const char* snt_last_cuda_error(void);
 uint32_t snt_abi_version(void);
 /* Diagnostic: kernels launched by this library in this process so far. */
 uint64_t snt_debug_launch_count(void);
-/* How snt_merkle_inplace / snt_merkle_leaves schedule their work (process-wide; returns the previous
+/* How snt_merkle_inplace / snt_merkle_leaves / snt_lthash_* schedule their work (process-wide; returns the previous
  * setting, an unknown value changes nothing). All three give bit-identical results.
  *   SNT_SCHEDULE_PERSISTENT (default): one persistent CTA per SM, leaves hashed in warp-wide chains with a
  *       time-sliced tail (csrc/merkle_fused.cuh), then the level-reducer launches. Fastest on every measured
@@ -54,7 +54,10 @@ uint64_t snt_debug_launch_count(void);
  *   SNT_SCHEDULE_FUSED: the same leaf scheduling with the tree folded into the SAME launch through
  *       completion counters -- one launch per hash (needs >= 5 levels and an initialised workspace,
  *       otherwise falls back to PERSISTENT).
- *   SNT_SCHEDULE_GRID: one thread per leaf on a plain grid, then the level reducer (round 1's path). */
+ *   SNT_SCHEDULE_GRID: one thread per leaf (or sample) on a plain grid, then the level reducer (round 1's
+ *       path).
+ * The LtHash entry points pick between their plain grid and their persistent chain kernel by item length
+ * and launch size under PERSISTENT; FUSED forces the chain kernel, GRID the grid. */
 typedef enum snt_schedule { SNT_SCHEDULE_PERSISTENT = 0, SNT_SCHEDULE_FUSED = 1, SNT_SCHEDULE_GRID = 2 } snt_schedule;
 int snt_merkle_schedule(int schedule);
 /* Diagnostic: a device buffer of 6 x u64 per SM (zeroed by the caller) into which every persistent CTA of
@@ -142,34 +145,35 @@ int snt_merkle_root(int alg, const void* d_nodes, uint64_t count, void* d_work, 
                     void* d_root, snt_stream_t stream);
 
 /* ---- LtHash ------------------------------------------------------------------
- * Accumulators are n_sources x 32 u32 lanes (sums modulo 2^32 of the u16
- * lanes; exact modulo 2^16 after snt_lt_finalize) plus n_sources u64 counts.
- * Calls ADD into d_acc / d_counts (zero them first for a fresh digest), so
+ * Accumulators are n_sources x 32 u64 lanes (sums modulo 2^64 of the u16
+ * lanes; exact modulo 2^16 after snt_lt_finalize), n_sources u64 counts and a
+ * u64 status word. Calls ADD into them (zero them first for a fresh digest), so
  * batches stream through the same accumulators (SourceAccumulator,
- * dataset.py:52-71) and partial accumulators from several GPUs combine with
- * one u32 sum all-reduce.
+ * dataset.py:52-71). Everything is u64 so that a caller can keep lanes, counts
+ * and status in ONE array and combine the partial accumulators of several GPUs
+ * with a single 64-bit sum all-reduce, nothing packed or unpacked.
  */
 
 /* process_batch / hash_sample (dataset.py:41-49, :74-86): sample i is
  * d_shard[d_off[i] .. +d_len[i]], digest BLAKE2b-512(LE64(d_ids[i]) || sample),
- * added into source slot d_slot[i]. A slot >= n_sources sets bit 0 of
- * *d_status (if not NULL) and the sample is skipped (undeclared source).
+ * added into source slot d_slot[i]. A sample whose slot is >= n_sources is
+ * skipped and counted in *d_status (if not NULL): non-zero = undeclared source.
  * d_digests, if not NULL, receives the n x 64 per-sample digests. */
 int snt_lthash_samples(const void* d_shard, const uint64_t* d_off, const uint64_t* d_len,
                        const uint64_t* d_ids, const uint32_t* d_slot, uint64_t n,
-                       uint32_t n_sources, uint32_t* d_acc, uint64_t* d_counts, void* d_digests,
-                       uint32_t* d_status, snt_stream_t stream);
+                       uint32_t n_sources, uint64_t* d_acc, uint64_t* d_counts, void* d_digests,
+                       uint64_t* d_status, snt_stream_t stream);
 
 /* inplace_hash, LATTICE construction (model.py:312-315): leaves
  * [leaf_begin, leaf_end) tagged LE64(k), summed into d_acc[32] / d_counts[1]. */
 int snt_lthash_model(const snt_model_plan* plan, uint64_t leaf_begin, uint64_t leaf_end,
-                     uint32_t* d_acc, uint64_t* d_counts, void* d_digests, snt_stream_t stream);
+                     uint64_t* d_acc, uint64_t* d_counts, void* d_digests, snt_stream_t stream);
 
 /* per_layer_hash, LATTICE construction (model.py:255-262): block j of tensor i is
  * tagged LE64(i) || LE64(j) and added into slot i of d_acc[n_tensors x 32] /
  * d_counts[n_tensors]; an empty tensor keeps the zero digest. */
 int snt_lthash_model_layers(const snt_model_plan* plan, uint64_t leaf_begin, uint64_t leaf_end,
-                            uint32_t* d_acc, uint64_t* d_counts, void* d_digests,
+                            uint64_t* d_acc, uint64_t* d_counts, void* d_digests,
                             snt_stream_t stream);
 
 /* per_layer_hash, MERKLE construction (model.py:245-253): one tree per segment.
@@ -196,11 +200,11 @@ int snt_gather_spans(const uint64_t* d_src_addr, const uint64_t* d_len, const ui
                      uint32_t pad_block, void* d_dst, snt_stream_t stream);
 
 /* lt_reduce (lattice.py:104-119): add n 64-byte digests into d_acc[32]. */
-int snt_lt_reduce(const void* d_digests, uint64_t n, uint32_t* d_acc, snt_stream_t stream);
+int snt_lt_reduce(const void* d_digests, uint64_t n, uint64_t* d_acc, snt_stream_t stream);
 
 /* Mask to 16 bits and pack: d_out receives n_sources x 64 bytes
  * (LatticeDigest layout, lattice.py:37-58). */
-int snt_lt_finalize(const uint32_t* d_acc, uint32_t n_sources, void* d_out, snt_stream_t stream);
+int snt_lt_finalize(const uint64_t* d_acc, uint32_t n_sources, void* d_out, snt_stream_t stream);
 
 #ifdef __cplusplus
 }

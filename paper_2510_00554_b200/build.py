@@ -100,8 +100,36 @@ def build_intpeak(force: bool = False) -> Path:
     return INTPEAK_BIN
 
 
+REFERENCE_SRC = Path("/root/reference/pkg/src/sentinel")
+REFERENCE_COPY = ORACLE_DIR / "_ref" / "sentinel"
+
+
+def stage_reference(force: bool = False) -> Path:
+    """Put the UNMODIFIED reference package where the GPU box can import it: ``oracle/_ref/sentinel``.
+
+    The reference is pure Python, so "building" it is a copy of its package directory from the read-only
+    tree it lives in. ``oracle/_ref/`` is git-ignored (no reference source enters the history) but travels
+    with the snapshot, exactly like the built ``.so`` files. Only ``bench.py`` (the ``--impl reference`` arm
+    and the ``cpu_baseline`` leg) and the tests import it, always as the thing measured against or checked
+    with -- never by the product. Where ``/root/reference`` does not exist (the GPU box) this is a no-op
+    and whatever travelled is used.
+    """
+    if not REFERENCE_SRC.is_dir():
+        return REFERENCE_COPY
+    newest = max(p.stat().st_mtime for p in REFERENCE_SRC.glob("*.py"))
+    if not force and REFERENCE_COPY.is_dir() and all((REFERENCE_COPY / p.name).exists() for p in REFERENCE_SRC.glob("*.py")) \
+            and min(p.stat().st_mtime for p in REFERENCE_COPY.glob("*.py")) >= newest:
+        return REFERENCE_COPY
+    if REFERENCE_COPY.exists():
+        shutil.rmtree(REFERENCE_COPY)
+    REFERENCE_COPY.parent.mkdir(parents=True, exist_ok=True)
+    shutil.copytree(REFERENCE_SRC, REFERENCE_COPY, ignore=shutil.ignore_patterns("__pycache__"))
+    return REFERENCE_COPY
+
+
 def build_all(force: bool = False) -> None:
     build_native(force)
+    stage_reference(force)
     if (ORACLE_DIR / "oracle.c").exists():
         build_oracle(force)
     if (HOSTCHECK_DIR / "hostcheck.cu").exists():

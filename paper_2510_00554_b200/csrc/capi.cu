@@ -476,21 +476,56 @@ int launch_blocks(const uint8_t* base, const uint64_t* off, const uint64_t* len,
     return SNT_OK;
 }
 
+template <class Items, bool SMEM_ACC>
+int launch_lthash_chains(const Items& items, uint64_t n, uint32_t n_sources, unsigned long long* acc,
+                         unsigned long long* counts, uint8_t* dig, unsigned long long* status, cudaStream_t s) {
+    const size_t smem = LT_CHAIN_STAGE_BYTES + LT_CHAIN_PARK_BYTES +
+                        (SMEM_ACC ? static_cast<size_t>(n_sources) * (LT_LANES + 1) * sizeof(uint32_t) : 0);
+    static const cudaError_t attr = cudaFuncSetAttribute(
+        lthash_chain_kernel<Items, SMEM_ACC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        static_cast<int>(LT_CHAIN_STAGE_BYTES + LT_CHAIN_PARK_BYTES + LT_SMEM_SOURCES * (LT_LANES + 1) * sizeof(uint32_t)));
+    if (attr != cudaSuccess) return cuda_fail(attr, "cudaFuncSetAttribute(lthash_chain_kernel)");
+    const uint64_t chains = (n + 31) >> 5;
+    const uint64_t sms = static_cast<uint64_t>(sm_count());
+    const unsigned grid = static_cast<unsigned>(chains < sms ? chains : sms);
+    int warps = static_cast<int>((chains / grid) & ~3ull);
+    warps = warps < 4 ? 4 : (warps > LT_CHAIN_MAXW ? LT_CHAIN_MAXW : warps);
+    lthash_chain_kernel<Items, SMEM_ACC><<<grid, warps * 32, smem, s>>>(items, n, n_sources, acc, counts, dig, status);
+    SNT_CUDA(cudaGetLastError());
+    ++g_launches;
+    return SNT_OK;
+}
+
 template <class Items>
-int launch_lthash(const Items& items, uint64_t n, uint32_t n_sources, uint32_t* d_acc,
-                  uint64_t* d_counts, void* d_digests, uint32_t* d_status, cudaStream_t s) {
+int launch_lthash(const Items& items, uint64_t n, uint32_t n_sources, uint64_t* d_acc,
+                  uint64_t* d_counts, void* d_digests, uint64_t* d_status, cudaStream_t s) {
     if (n == 0) return SNT_OK;
     auto* counts = reinterpret_cast<unsigned long long*>(d_counts);
+    auto* acc = reinterpret_cast<unsigned long long*>(d_acc);
+    auto* status = reinterpret_cast<unsigned long long*>(d_status);
     auto* dig = static_cast<uint8_t*>(d_digests);
+    const bool smem_acc = n_sources <= static_cast<uint32_t>(LT_SMEM_SOURCES);
+    // Persistent CTAs with warp-wide chains and a time-sliced tail (lthash_chain_kernel) pay a queue operation
+    // and a pipeline restart per slice. That is worth it only for long items in a launch of a wave or two --
+    // model blocks (8 KiB = 65 BLAKE2b blocks each), where the plain grid loses a whole warp-time to
+    // quantisation: GPT-2 small LATTICE 0.713 -> 0.664 ms. Dataset samples are short (CIFAR 25 blocks,
+    // hellaswag ~3): there the plain grid wins (CIFAR 194 vs 210 us, 2 M ragged samples 1.26 vs 2.82 ms;
+    // tools/lthash_probe.py, tools/lthash_big_probe.py), so samples always take it.
+    const uint64_t chains_per_sm = ((n + 31) >> 5) / static_cast<uint64_t>(sm_count());
+    const int schedule = g_schedule.load();           // FUSED forces the chain kernel (tests, A/B timing), GRID the grid
+    if (schedule == SNT_SCHEDULE_FUSED || (Items::LONG_ITEMS && chains_per_sm < 32 && schedule != SNT_SCHEDULE_GRID)) {
+        if (smem_acc) return launch_lthash_chains<Items, true>(items, n, n_sources, acc, counts, dig, status, s);
+        return launch_lthash_chains<Items, false>(items, n, n_sources, acc, counts, dig, status, s);
+    }
     const uint64_t grid = (n + LT_THREADS - 1) / LT_THREADS;
     if (grid > 0x7fffffffull) return SNT_ERR_INVALID_INPUT;
-    if (n_sources <= static_cast<uint32_t>(LT_SMEM_SOURCES)) {
+    if (smem_acc) {
         const size_t smem = LT_STAGE_BYTES + static_cast<size_t>(n_sources) * (LT_LANES + 1) * sizeof(uint32_t);
         lthash_kernel<Items, true><<<static_cast<unsigned>(grid), LT_THREADS, smem, s>>>(
-            items, n, n_sources, d_acc, counts, dig, d_status);
+            items, n, n_sources, acc, counts, dig, status);
     } else {
         lthash_kernel<Items, false><<<static_cast<unsigned>(grid), LT_THREADS, LT_STAGE_BYTES, s>>>(
-            items, n, n_sources, d_acc, counts, dig, d_status);
+            items, n, n_sources, acc, counts, dig, status);
     }
     SNT_CUDA(cudaGetLastError());
     ++g_launches;
@@ -589,7 +624,7 @@ int snt_merkle_root(int alg, const void* d_nodes, uint64_t count, void* d_work, 
 
 int snt_lthash_samples(const void* d_shard, const uint64_t* d_off, const uint64_t* d_len,
                        const uint64_t* d_ids, const uint32_t* d_slot, uint64_t n, uint32_t n_sources,
-                       uint32_t* d_acc, uint64_t* d_counts, void* d_digests, uint32_t* d_status,
+                       uint64_t* d_acc, uint64_t* d_counts, void* d_digests, uint64_t* d_status,
                        snt_stream_t stream) {
     if (n_sources == 0 || !d_acc || !d_counts) return SNT_ERR_INVALID_INPUT;
     if (n && (!d_off || !d_len || !d_ids || !d_slot)) return SNT_ERR_INVALID_INPUT;
@@ -603,7 +638,7 @@ int snt_lthash_samples(const void* d_shard, const uint64_t* d_off, const uint64_
                          static_cast<cudaStream_t>(stream));
 }
 
-int snt_lthash_model(const snt_model_plan* plan, uint64_t leaf_begin, uint64_t leaf_end, uint32_t* d_acc,
+int snt_lthash_model(const snt_model_plan* plan, uint64_t leaf_begin, uint64_t leaf_end, uint64_t* d_acc,
                      uint64_t* d_counts, void* d_digests, snt_stream_t stream) {
     if (!plan || !d_acc || !d_counts) return SNT_ERR_INVALID_INPUT;
     if (leaf_begin > leaf_end || leaf_end > plan->n_leaves) return SNT_ERR_INVALID_INPUT;
@@ -614,7 +649,7 @@ int snt_lthash_model(const snt_model_plan* plan, uint64_t leaf_begin, uint64_t l
                          static_cast<cudaStream_t>(stream));
 }
 
-int snt_lthash_model_layers(const snt_model_plan* plan, uint64_t leaf_begin, uint64_t leaf_end, uint32_t* d_acc,
+int snt_lthash_model_layers(const snt_model_plan* plan, uint64_t leaf_begin, uint64_t leaf_end, uint64_t* d_acc,
                             uint64_t* d_counts, void* d_digests, snt_stream_t stream) {
     if (!plan || !d_acc || !d_counts) return SNT_ERR_INVALID_INPUT;
     if (leaf_begin > leaf_end || leaf_end > plan->n_leaves) return SNT_ERR_INVALID_INPUT;
@@ -703,23 +738,23 @@ int snt_gather_spans(const uint64_t* d_src_addr, const uint64_t* d_len, const ui
     return SNT_OK;
 }
 
-int snt_lt_reduce(const void* d_digests, uint64_t n, uint32_t* d_acc, snt_stream_t stream) {
+int snt_lt_reduce(const void* d_digests, uint64_t n, uint64_t* d_acc, snt_stream_t stream) {
     if (!d_acc || (n && !d_digests)) return SNT_ERR_INVALID_INPUT;
     if (n == 0) return SNT_OK;                                                        // lattice.py:112-113
     uint64_t grid = (n + 63) / 64;
     if (grid > 148 * 8) grid = 148 * 8;
     lt_reduce_kernel<<<static_cast<unsigned>(grid), 256, 0, static_cast<cudaStream_t>(stream)>>>(
-        static_cast<const uint8_t*>(d_digests), n, d_acc);
+        static_cast<const uint8_t*>(d_digests), n, reinterpret_cast<unsigned long long*>(d_acc));
     SNT_CUDA(cudaGetLastError());
     ++g_launches;
     return SNT_OK;
 }
 
-int snt_lt_finalize(const uint32_t* d_acc, uint32_t n_sources, void* d_out, snt_stream_t stream) {
+int snt_lt_finalize(const uint64_t* d_acc, uint32_t n_sources, void* d_out, snt_stream_t stream) {
     if (!d_acc || !d_out || n_sources == 0) return SNT_ERR_INVALID_INPUT;
     const uint32_t n_words = n_sources * (LT_LANES / 2);
     lt_finalize_kernel<<<(n_words + 255) / 256, 256, 0, static_cast<cudaStream_t>(stream)>>>(
-        d_acc, n_words, static_cast<uint32_t*>(d_out));
+        reinterpret_cast<const unsigned long long*>(d_acc), n_words, static_cast<uint32_t*>(d_out));
     SNT_CUDA(cudaGetLastError());
     ++g_launches;
     return SNT_OK;

@@ -33,11 +33,11 @@
 // packed 32 to a chain of their own, hashed through the out-of-line generic path at the front of an
 // SM's queue, and signal their groups leaf by leaf.
 #pragma once
+#include "chain_sched.cuh"
 #include "merkle_kernels.cuh"
 
 namespace snt {
 
-constexpr int FUSED_RING = 64;             // parked-chain FIFO capacity (needs 2 * W - 1, W <= 32)
 constexpr int FUSED_MAX_STAGES = 8;
 constexpr uint32_t FUSED_MIN_LEVELS = 5;   // a chain (32 leaves) must lie inside one first-stage group
 constexpr uint32_t FUSED_FIRST_STAGE_LEVELS = 8;
@@ -69,23 +69,6 @@ SNT_D unsigned long long fused_now_ns() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
     return t;
-}
-
-struct FusedSched {
-    int lock;
-    int fresh;                               // next chain of this CTA that has not been started
-    int head, tail;                          // FIFO of parked chains
-    int ring[FUSED_RING];
-    int prog[FUSED_RING];                    // units done, per slot of the time-sliced group
-};
-
-SNT_D void sched_lock(FusedSched* sc) {
-    while (atomicCAS(&sc->lock, 0, 1) != 0) {}
-    __threadfence_block();
-}
-SNT_D void sched_unlock(FusedSched* sc) {
-    __threadfence_block();
-    atomicExch(&sc->lock, 0);
 }
 
 // A parked chain keeps, per lane, the hash state and where its leaf is (address, length, whether the lane
@@ -261,11 +244,7 @@ SNT_D void fused_climb(const FusedArgs& a, const MerkleConsts* c, const FusedSch
     for (;;) {
         __threadfence();
         // leaf chains still queued on this SM? then tread lightly on the instruction cache
-        int busy = 0;
-        if (lane == 0)
-            busy = (*reinterpret_cast<const volatile int*>(&sc->fresh) < count) ||
-                   (*reinterpret_cast<const volatile int*>(&sc->head) != *reinterpret_cast<const volatile int*>(&sc->tail));
-        const bool small = __shfl_sync(0xffffffffu, busy, 0) != 0;
+        const bool small = sched_waiting(sc, count, lane);
         if (a.trace && lane == 0) atomicAdd(a.trace + 6ull * blockIdx.x + 2, 1ull);
         const uint8_t* children = (stage == 0 ? a.d_leaves : a.tree.nodes[stage - 1]) +
                                   ((g << a.tree.m[stage]) * A::DIGEST_BYTES);
@@ -329,33 +308,22 @@ merkle_fused_kernel(const __grid_constant__ FusedArgs a, const __grid_constant__
     if (bid >= light_first && bid - light_first < n_irr_chains)
         n_irr = static_cast<int>((n_irr_chains - (bid - light_first) + n_light - 1) / n_light);
     const int count = n_irr + n_reg;
-    const int first_sliced = count > W ? count - W - (count % W) : count;
+    const int first_sliced = sched_first_sliced(count, W);
     const uint32_t units = fused_units<ALG>(a.tab.block_shift);
     const uint32_t slice = (units + W - 1) / W;
 
-    if (threadIdx.x == 0) {
-        sc.lock = 0; sc.fresh = 0; sc.head = 0; sc.tail = 0;
-        if (a.trace) {
-            uint32_t smid;
-            asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
-            a.trace[6ull * blockIdx.x] = fused_now_ns();
-            a.trace[6ull * blockIdx.x + 5] = smid;
-        }
+    if (threadIdx.x == 0 && a.trace) {
+        uint32_t smid;
+        asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+        a.trace[6ull * blockIdx.x] = fused_now_ns();
+        a.trace[6ull * blockIdx.x + 5] = smid;
     }
-    if (threadIdx.x < FUSED_RING) sc.prog[threadIdx.x] = 0;
-    __syncthreads();
+    sched_init(&sc);
     uint32_t* const my_park = reinterpret_cast<uint32_t*>(fused_smem + fused_stage_bytes<ALG, MAXW>());
     const uint32_t m0 = a.tree.n_stages ? a.tree.m[0] : 0;
 
     for (;;) {
-        int ch = -1;
-        if (lane == 0) {
-            sched_lock(&sc);
-            if (sc.fresh < count) ch = sc.fresh++;
-            else if (sc.head != sc.tail) ch = sc.ring[(sc.head++) & (FUSED_RING - 1)];
-            sched_unlock(&sc);
-        }
-        ch = __shfl_sync(0xffffffffu, ch, 0);
+        const int ch = sched_pop(&sc, count, lane);
         if (ch < 0) break;
         if (a.trace && lane == 0) atomicAdd(a.trace + 6ull * blockIdx.x + 3, 1ull);
 
@@ -451,26 +419,14 @@ merkle_fused_kernel(const __grid_constant__ FusedArgs a, const __grid_constant__
             __syncwarp();
             if (u1 == units) break;
             u0 = u1;
-            // is anybody waiting for a warp? if not, keep going with this chain
-            int waiting = 0;
-            if (lane == 0)
-                waiting = (*reinterpret_cast<volatile int*>(&sc.fresh) < count) ||
-                          (*reinterpret_cast<volatile int*>(&sc.head) != *reinterpret_cast<volatile int*>(&sc.tail));
-            if (!__shfl_sync(0xffffffffu, waiting, 0)) continue;
+            if (!sched_waiting(&sc, count, lane)) continue;      // nobody is waiting for a warp: keep this chain
 #pragma unroll
             for (int i = 0; i < SW; ++i) st[i * 32] = s[i];
             st[SW * 32] = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(leaf.ptr));
             st[(SW + 1) * 32] = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(leaf.ptr) >> 32);
             st[(SW + 2) * 32] = static_cast<uint32_t>(leaf.len);          // a leaf is at most one block (< 2^32 bytes)
             st[(SW + 3) * 32] = valid ? 1u : 0u;
-            __threadfence_block();
-            __syncwarp();
-            if (lane == 0) {
-                sched_lock(&sc);
-                sc.prog[slot] = static_cast<int>(u0);
-                sc.ring[(sc.tail++) & (FUSED_RING - 1)] = ch;
-                sched_unlock(&sc);
-            }
+            sched_park(&sc, ch, slot, u0, lane);
             parked = true;
             break;
         }

@@ -32,7 +32,20 @@ from .errors import FormatError, ValidationError
 from .lattice import LatticeDigest, lt_add, lt_hash_block, lt_hash_tagged, lt_zero
 
 
-BALANCE_MIN_SAMPLES = 1 << 18        # ragged datasets at least this large are hashed in length-sorted order
+# Ragged datasets at least this large are hashed in length-sorted order. Measured on B200 with 2 M
+# hellaswag-shaped samples (tools/lthash_big_probe.py): the LtHash launch 2.93 -> 1.26 ms, the device argsort +
+# four row gathers 0.42 ms warm (the first argsort of a process also pays torch's one-time ~0.3 s sort set-up),
+# i.e. the sort pays for itself from roughly half a million samples; below a million it is not worth a branch.
+BALANCE_MIN_SAMPLES = 1 << 20
+
+
+def _checked_ids(ids) -> np.ndarray:
+    """Sample ids as u64; an id outside [0, 2^64) is an error, as it is for the reference's
+    ``struct.pack("<Q", sample_id)`` (dataset.py:45) -- never wrapped into another sample's tag."""
+    for i in ids:
+        if not 0 <= i < (1 << 64):
+            raise ValidationError(f"sample id {i} does not fit an unsigned 64-bit tag")
+    return np.array(ids, dtype=np.uint64)
 
 
 @dataclass(frozen=True)
@@ -61,14 +74,126 @@ def hash_sample(s: SampleRecord, cover_labels: bool = False) -> LatticeDigest:
     return lt_hash_block(s.sample_id, s.data)
 
 
-@dataclass
-class SourceAccumulator:
-    """Per-source running lattice sums and sample counts (host mirror, dataset.py:52-71)."""
+class _BatchEngine:
+    """Device side of a ``SourceAccumulator`` that is fed batch by batch (``process_batch``).
 
-    sums: Dict[int, LatticeDigest] = field(default_factory=dict)
-    counts: Dict[int, int] = field(default_factory=dict)
-    declared_sources: Optional[frozenset] = None
-    cover_labels: bool = False
+    Everything a batch needs travels as ONE block: ``offsets | lengths | ids | slots | sample bytes`` is
+    packed into a pinned staging buffer (two of them, used alternately, each re-used once the copy that
+    read it has completed), goes to a persistent device buffer with one asynchronous copy, and one
+    ``snt_lthash_samples`` launch adds the batch into per-source lane sums that stay in HBM. Nothing is
+    allocated per batch and nothing synchronises until the sums are asked for (``drain``).
+    """
+
+    HEADER_ALIGN = 16
+
+    def __init__(self):
+        self.device = _dev.require_cuda()
+        self.slot_of: Dict[int, int] = {}
+        self.capacity = 32
+        self.acc = _dev.LatticeAccumulator(self.capacity)
+        self.stage: List[Optional[torch.Tensor]] = [None, None]
+        self.stage_done: List[Optional[torch.cuda.Event]] = [None, None]
+        self.turn = 0
+        self.d_block: Optional[torch.Tensor] = None
+        self.pending = False
+
+    def _slot(self, sid: int) -> int:
+        slot = self.slot_of.get(sid)
+        if slot is None:
+            slot = len(self.slot_of)
+            if slot >= self.capacity:                      # more sources than slots: carry the sums over to a bigger state
+                grown = _dev.LatticeAccumulator(self.capacity * 4)
+                n = self.capacity
+                grown.acc[:n * _dev.LT_LANES].copy_(self.acc.acc)
+                grown.counts[:n].copy_(self.acc.counts)
+                grown.status.copy_(self.acc.status)
+                self.acc, self.capacity = grown, self.capacity * 4
+            self.slot_of[sid] = slot
+        return slot
+
+    def add(self, payloads: Sequence[bytes], ids: np.ndarray, source_ids: Sequence[int]) -> None:
+        n = len(payloads)
+        lengths = np.fromiter((len(p) for p in payloads), dtype=np.uint64, count=n)
+        total = int(lengths.sum())
+        header = -(-28 * n // self.HEADER_ALIGN) * self.HEADER_ALIGN
+        need = header + max(total, 16)
+        turn = self.turn
+        self.turn ^= 1
+        if self.stage[turn] is None or self.stage[turn].numel() < need:
+            self.stage[turn] = torch.empty(max(need * 2, 1 << 20), dtype=torch.uint8, pin_memory=True)
+            self.stage_done[turn] = None
+        if self.stage_done[turn] is not None:
+            self.stage_done[turn].synchronize()            # the copy that last read this staging buffer
+        if self.d_block is None or self.d_block.numel() < need:
+            self.d_block = torch.empty(max(need * 2, 1 << 20), dtype=torch.uint8, device=self.device)
+        view = self.stage[turn].numpy()
+        offsets = view[0:8 * n].view(np.uint64)
+        offsets[0] = 0
+        np.cumsum(lengths[:-1], out=offsets[1:])
+        view[8 * n:16 * n].view(np.uint64)[:] = lengths
+        view[16 * n:24 * n].view(np.uint64)[:] = ids
+        view[24 * n:28 * n].view(np.int32)[:] = [self._slot(s) for s in source_ids]
+        view[header:header + total] = np.frombuffer(b"".join(payloads), dtype=np.uint8)
+        d = self.d_block
+        d[:need].copy_(self.stage[turn][:need], non_blocking=True)
+        done = torch.cuda.Event()
+        done.record()
+        self.stage_done[turn] = done
+        self.acc.add_samples(d[header:], d[0:8 * n].view(torch.int64), d[8 * n:16 * n].view(torch.int64),
+                             d[16 * n:24 * n].view(torch.int64), d[24 * n:28 * n].view(torch.int32))
+        self.pending = True
+
+    def drain(self) -> Dict[int, Tuple[bytes, int]]:
+        """Per-source (64 digest bytes, count) accumulated since the last drain; synchronises, then starts from zero."""
+        out, counts, status = self.acc.digests()
+        if status:
+            raise ValidationError("a sample references an undeclared source")
+        self.acc.zero_()
+        self.pending = False
+        return {sid: (out[64 * slot:64 * slot + 64], counts[slot]) for sid, slot in self.slot_of.items() if counts[slot]}
+
+
+class SourceAccumulator:
+    """Per-source running lattice sums and sample counts (mirror of dataset.py:52-71).
+
+    ``process_batch`` keeps the running sums on the device (``_BatchEngine``); ``sums`` and ``counts``
+    are the reference's host dictionaries and fold the device state in whenever they are read, so the
+    object behaves like the reference's dataclass while a loader loop never waits for the GPU.
+    """
+
+    def __init__(self, sums: Optional[Dict[int, LatticeDigest]] = None, counts: Optional[Dict[int, int]] = None,
+                 declared_sources: Optional[frozenset] = None, cover_labels: bool = False):
+        self._sums: Dict[int, LatticeDigest] = {} if sums is None else sums
+        self._counts: Dict[int, int] = {} if counts is None else counts
+        self.declared_sources = declared_sources
+        self.cover_labels = cover_labels
+        self._engine: Optional[_BatchEngine] = None
+
+    def _sync(self) -> None:
+        if self._engine is not None and self._engine.pending:
+            for sid, (digest, count) in self._engine.drain().items():
+                self._sums[sid] = lt_add(self._sums.get(sid, lt_zero()), LatticeDigest(digest))
+                self._counts[sid] = self._counts.get(sid, 0) + count
+
+    @property
+    def sums(self) -> Dict[int, LatticeDigest]:
+        self._sync()
+        return self._sums
+
+    @sums.setter
+    def sums(self, value: Dict[int, LatticeDigest]) -> None:
+        self._sync()
+        self._sums = value
+
+    @property
+    def counts(self) -> Dict[int, int]:
+        self._sync()
+        return self._counts
+
+    @counts.setter
+    def counts(self, value: Dict[int, int]) -> None:
+        self._sync()
+        self._counts = value
 
     def declare(self, source_ids: Iterable[int]) -> None:
         self.declared_sources = frozenset(source_ids)
@@ -81,6 +206,16 @@ class SourceAccumulator:
         for sid, digest in other.sums.items():
             self.sums[sid] = lt_add(self.sums.get(sid, lt_zero()), digest)
             self.counts[sid] = self.counts.get(sid, 0) + other.counts.get(sid, 0)
+
+    def __repr__(self) -> str:
+        return (f"SourceAccumulator(sums={self.sums!r}, counts={self.counts!r}, "
+                f"declared_sources={self.declared_sources!r}, cover_labels={self.cover_labels!r})")
+
+    def __eq__(self, other) -> bool:
+        if not isinstance(other, SourceAccumulator):
+            return NotImplemented
+        return (self.sums, self.counts, self.declared_sources, self.cover_labels) == \
+               (other.sums, other.counts, other.declared_sources, other.cover_labels)
 
 
 class DeviceDataset:
@@ -143,8 +278,8 @@ class DeviceDataset:
         One thread hashes one sample, so a warp runs as long as its longest sample: with ragged
         samples in arrival order half of the lanes idle. Per-source sums do not depend on the order
         (dataset.py:67-71), so sorting the rows is free of semantics and makes every warp's lanes run
-        the same number of BLAKE2b compressions (2 M hellaswag-shaped samples: 2.94 -> 1.26 ms,
-        tools/ragged_probe.py). Worth its ~0.5 ms only for large ragged datasets.
+        the same number of BLAKE2b compressions (2 M hellaswag-shaped samples: 2.93 -> 1.26 ms for 0.42 ms of
+        sorting, tools/lthash_big_probe.py). Worth it only for large ragged datasets (BALANCE_MIN_SAMPLES).
         """
         order = torch.argsort(self.lengths)
         return DeviceDataset(self.shard, self.offsets[order], self.lengths[order], self.ids[order], self.slots[order],
@@ -162,33 +297,28 @@ class DeviceDataset:
 
 def _finalize_device(acc: "_dev.LatticeAccumulator", source_ids: Sequence[int]) -> Dict[int, Tuple[LatticeDigest, int]]:
     out, counts, status = acc.digests()
-    if status & 1:
+    if status:
         raise ValidationError("a sample references an undeclared source")
     return {sid: (LatticeDigest(out[64 * i:64 * i + 64]), counts[i]) for i, sid in enumerate(source_ids)}
 
 
 def process_batch(batch: Batch, acc: SourceAccumulator) -> SourceAccumulator:
-    """Hash a batch on the GPU, reduce it per source, add to the running sums (dataset.py:74-86)."""
-    present: List[int] = []
+    """Hash a batch on the GPU and add it to the running per-source sums (dataset.py:74-86).
+
+    The batch is packed into a reused pinned block, copied with one asynchronous transfer and hashed by
+    one launch into sums that stay on the device; the call returns without waiting for the GPU. The
+    host-side ``acc.sums`` / ``acc.counts`` catch up when they are read (``finalize`` does).
+    """
     for s in batch.samples:
         if acc.declared_sources is not None and s.source_id not in acc.declared_sources:
             raise ValidationError(f"sample {s.sample_id} references undeclared source {s.source_id}")
-        if s.source_id not in present:
-            present.append(s.source_id)
     if not batch.samples:
         return acc
     payloads = [(s.label + s.data) if acc.cover_labels else s.data for s in batch.samples]
-    lengths = np.fromiter((len(p) for p in payloads), dtype=np.uint64, count=len(payloads))
-    offsets = np.zeros(len(payloads), dtype=np.uint64)
-    np.cumsum(lengths[:-1], out=offsets[1:])
-    ids = np.array([s.sample_id & 0xFFFFFFFFFFFFFFFF for s in batch.samples], dtype=np.uint64)
-    ds = DeviceDataset.from_host(b"".join(payloads), offsets, lengths, ids,
-                                 [s.source_id for s in batch.samples], present)
-    dacc = _dev.LatticeAccumulator(len(ds.source_ids))
-    ds.accumulate(dacc)
-    for sid, (digest, count) in _finalize_device(dacc, ds.source_ids).items():
-        acc.sums[sid] = lt_add(acc.sums.get(sid, lt_zero()), digest)
-        acc.counts[sid] = acc.counts.get(sid, 0) + count
+    ids = _checked_ids([s.sample_id for s in batch.samples])
+    if acc._engine is None:
+        acc._engine = _BatchEngine()
+    acc._engine.add(payloads, ids, [s.source_id for s in batch.samples])
     return acc
 
 
@@ -271,7 +401,7 @@ def digest_dataset(manifest: DatasetManifest, batch_size: int = 128, shuffle_see
     source_ids = sorted(manifest.source_ids)
     if n == 0:
         return {}
-    ids = np.array([r[0] & 0xFFFFFFFFFFFFFFFF for r in manifest.samples], dtype=np.uint64)
+    ids = _checked_ids([r[0] for r in manifest.samples])
     src = np.array([r[1] for r in manifest.samples], dtype=np.int64)
     off = np.array([r[3] for r in manifest.samples], dtype=np.int64)
     ln = np.array([r[4] for r in manifest.samples], dtype=np.int64)
@@ -350,4 +480,4 @@ class StreamingDatasetHasher:
         """Combine the per-rank sums of a data-parallel job (one all-reduce, see distributed.py)."""
         from . import distributed as _dd
 
-        _dd.allreduce_lattice(self._acc.acc, self._acc.counts, self._acc.status, group)
+        _dd.allreduce_lattice(self._acc.state, group)

@@ -110,9 +110,13 @@ class StagingRing:
 
     @classmethod
     def get(cls, threads: int) -> "StagingRing":
-        if cls._instance is None or cls._instance.threads < threads or \
-                cls._instance.bufs[0].numel() != STAGE_SLOT_BYTES or len(cls._instance.bufs) != STAGE_RING_SLOTS:
+        old = cls._instance
+        if old is None or old.threads < threads or \
+                old.bufs[0].numel() != STAGE_SLOT_BYTES or len(old.bufs) != STAGE_RING_SLOTS:
             cls._instance = cls(threads)
+            if old is not None:
+                with old.lock:                       # wait for a hash that still owns the old ring
+                    old.pool.shutdown(wait=True)
         return cls._instance
 
     def acquire(self) -> int:
@@ -482,6 +486,14 @@ def merkle_root_device(alg: str, nodes: torch.Tensor, count: int) -> torch.Tenso
     return root
 
 
+def merkle_root_into(alg: str, nodes: torch.Tensor, count: int, work: torch.Tensor, work_bytes: int,
+                     root: torch.Tensor) -> torch.Tensor:
+    """``snt_merkle_root`` with caller-owned workspace and root buffer (no allocation, no synchronisation)."""
+    rc = _native.load().snt_merkle_root(ALG_IDS[alg], _ptr(nodes), count, _ptr(work), work_bytes, _ptr(root), _stream())
+    _native.check(rc, "snt_merkle_root")
+    return root
+
+
 def merkle_reduce_levels_device(alg: str, nodes: torch.Tensor, first: int, n_in: int, level_count: int,
                                 levels: int) -> torch.Tensor:
     """``snt_merkle_reduce_levels``: apply ``levels`` tree levels to a node range."""
@@ -517,11 +529,14 @@ def merkle_roots_segmented_device(alg: str, digests: torch.Tensor, seg_first: Se
 
 
 class LatticeAccumulator:
-    """Device-resident per-source LtHash sums: ``n_sources x 32`` u32 lanes + u64 counts.
+    """Device-resident per-source LtHash sums: ``n_sources x 32`` u64 lanes, u64 counts, a status word.
 
     The running state of ``SourceAccumulator`` (reference dataset.py:52-71) kept
-    in HBM. Lanes are summed modulo 2^32 and masked to 16 bits by ``digests``;
-    that is exact modulo 2^16 for any number of samples.
+    in HBM as ONE int64 array ``state = [lanes | counts | status]`` (``acc``, ``counts`` and
+    ``status`` are views of it), so the partial accumulators of several GPUs combine with a
+    single sum all-reduce of ``state`` and nothing is packed or unpacked. Lanes are summed
+    modulo 2^64 and masked to 16 bits by ``digests``: exact modulo 2^16 for any number of
+    samples. ``status`` counts the samples that named an undeclared source.
     """
 
     def __init__(self, n_sources: int):
@@ -529,14 +544,14 @@ class LatticeAccumulator:
         if n_sources < 1:
             raise InvalidInput("at least one source slot is required")
         self.n_sources = n_sources
-        self.acc = torch.zeros(n_sources * LT_LANES, dtype=torch.int32, device=dev)
-        self.counts = torch.zeros(n_sources, dtype=torch.int64, device=dev)
-        self.status = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.state = torch.zeros(n_sources * (LT_LANES + 1) + 1, dtype=torch.int64, device=dev)
+        self.acc = self.state[:n_sources * LT_LANES]
+        self.counts = self.state[n_sources * LT_LANES:n_sources * (LT_LANES + 1)]
+        self.status = self.state[n_sources * (LT_LANES + 1):]
+        self._out_host: Optional[torch.Tensor] = None
 
     def zero_(self) -> None:
-        self.acc.zero_()
-        self.counts.zero_()
-        self.status.zero_()
+        self.state.zero_()
 
     def add_samples(self, shard: torch.Tensor, offsets: torch.Tensor, lengths: torch.Tensor,
                     ids: torch.Tensor, slots: torch.Tensor, digests: Optional[torch.Tensor] = None) -> None:
@@ -580,5 +595,5 @@ class LatticeAccumulator:
         out = torch.empty(self.n_sources * 64, dtype=torch.uint8, device=self.acc.device)
         rc = lib.snt_lt_finalize(_ptr(self.acc), self.n_sources, _ptr(out), _stream())
         _native.check(rc, "snt_lt_finalize")
-        return (out.cpu().numpy().tobytes(), [int(c) for c in self.counts.cpu().tolist()],
-                int(self.status.cpu().item()))
+        tail = self.state[self.n_sources * LT_LANES:].cpu().tolist()      # counts and status in one copy
+        return out.cpu().numpy().tobytes(), [int(c) for c in tail[:-1]], int(tail[-1])

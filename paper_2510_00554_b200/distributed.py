@@ -9,8 +9,9 @@ Each rank owns a contiguous run of whole shards; the only exchange is one
 all-gather of shard roots (a few KB).
 
 LtHash: lane sums are commutative (dataset.py:67-71), so each rank accumulates a
-contiguous sample range into ``n_sources x 32`` u32 lanes and one sum all-reduce
-combines them (u32 because NCCL has no u16 type; exact modulo 2^16).
+contiguous sample range into ``n_sources x 32`` widened lanes and one sum all-reduce
+combines them (widened to u64 because NCCL has no u16 type and so that lanes, counts and status
+share one array; exact modulo 2^16).
 
 The hashing itself is injected as a ``backend`` (CUDA in the product, see
 ``CudaBackend``); the partition / gather / top-reduce logic here is plain host
@@ -29,7 +30,6 @@ from .errors import InvalidInput
 from .workers import chunk_ranges
 
 DEFAULT_SHARD_LEVELS = 10   # 1024 leaves = 8 MiB of tensor bytes per shard
-STATUS_BITS = 4             # flag bits of LatticeAccumulator.status carried through the all-reduce
 
 
 def ceil_div(a: int, b: int) -> int:
@@ -109,19 +109,36 @@ class CudaBackend:
         return h.out_padded
 
     def gather_buffers(self, shard_plan: "ShardPlan", world: int, widest: int):
-        """Persistent receive buffer of the all-gather and the row index that compacts its slots
-        (rank r's first ``shard_count(r)`` rows) into shard order."""
+        """Persistent buffers of the exchange: the all-gather's receive buffer, the row index that compacts
+        its slots (rank r's first ``shard_count(r)`` rows) into shard order, and the compacted node array."""
         key = ("gather", shard_plan.n_shards, world, widest)
         got = self._hashers.get(key)
         if got is None:
             recv = torch.empty(world * widest * self.dlen, dtype=torch.uint8, device=self.device)
             rows = [r * widest + i for r in range(world) for i in range(shard_plan.shard_count(r))]
-            got = (recv, torch.tensor(rows, dtype=torch.int64, device=self.device))
+            nodes = torch.empty(len(rows), self.dlen, dtype=torch.uint8, device=self.device)
+            got = (recv, torch.tensor(rows, dtype=torch.int64, device=self.device), nodes)
             self._hashers[key] = got
         return got
 
+    def empty_slot(self, slots: int) -> torch.Tensor:
+        """The all-gather contribution of a rank that owns no shard (more ranks than shards)."""
+        key = ("empty", slots)
+        if key not in self._hashers:
+            self._hashers[key] = torch.zeros(slots * self.dlen, dtype=torch.uint8, device=self.device)
+        return self._hashers[key]
+
     def root_of(self, nodes: torch.Tensor, count: int) -> torch.Tensor:
-        return self._dev.merkle_root_device(self.alg, nodes, count)
+        """Ordinary tree rule over ``count`` level-k nodes; workspace and root buffer are kept per count."""
+        key = ("top", count)
+        got = self._hashers.get(key)
+        if got is None:
+            wb = self._dev.merkle_work_bytes(self.alg, count)
+            got = (torch.zeros(max(wb, 16), dtype=torch.uint8, device=self.device), wb,
+                   torch.empty(self.dlen, dtype=torch.uint8, device=self.device))
+            self._hashers[key] = got
+        work, wb, root = got
+        return self._dev.merkle_root_into(self.alg, nodes, count, work, wb, root)
 
     def to_bytes(self, t: torch.Tensor) -> bytes:
         return t.cpu().numpy().tobytes()
@@ -136,17 +153,22 @@ def _needs_host_staging(t: torch.Tensor, group=None) -> bool:
     return t.device.type == "cuda" and dist.get_backend(group) == "gloo"
 
 
-def sharded_merkle_root(backend, shard_plan: ShardPlan, rank: int, world: int, group=None) -> torch.Tensor:
+def sharded_merkle_root(backend, shard_plan: ShardPlan, rank: int, world: int, group=None,
+                        always_gather: bool = False) -> torch.Tensor:
     """This rank's shard roots -> all-gather -> top reduce. Returns the root (flat uint8 tensor).
 
-    Every rank returns the same root. With ``world == 1`` no collective is issued.
+    Every rank returns the same root. With ``world == 1`` no collective is issued unless
+    ``always_gather`` asks for the exchange anyway (a one-rank NCCL group exercises the very calls the
+    multi-GPU path makes). Nothing is allocated per call on the product path: send slot, receive
+    buffer, compaction index, node array, top-reduce workspace and root live in the backend.
     """
     dlen = backend.dlen
     begin, end = shard_plan.leaf_range(rank)
     mine = shard_plan.shard_count(rank)
-    fused_slot = world > 1 and hasattr(backend, "shard_roots_padded")
+    exchange = world > 1 or always_gather
+    fused_slot = exchange and hasattr(backend, "shard_roots_padded")
     local = backend.shard_roots(begin, end, shard_plan.levels) if (mine and not fused_slot) else None
-    if world == 1:
+    if not exchange:
         if shard_plan.n_shards == 1:
             return local                               # already the single level-k node = the root
         nodes = local
@@ -154,16 +176,18 @@ def sharded_merkle_root(backend, shard_plan: ShardPlan, rank: int, world: int, g
         # product path (NCCL): the leaf + shard-reduce launches write straight into the all-gather slot,
         # the receive buffer is persistent, one index_select puts the roots in shard order
         widest = max(shard_plan.shard_count(r) for r in range(world))
-        send = backend.shard_roots_padded(begin, end, shard_plan.levels, widest) if mine else \
-            torch.zeros(widest * dlen, dtype=torch.uint8, device=backend.device)
-        recv, rows = backend.gather_buffers(shard_plan, world, widest)
+        send = backend.shard_roots_padded(begin, end, shard_plan.levels, widest) if mine else backend.empty_slot(widest)
+        recv, rows, nodes2d = backend.gather_buffers(shard_plan, world, widest)
         if _needs_host_staging(send, group):           # debugging over gloo: same buffers, staged through the host
             host = torch.empty(recv.numel(), dtype=torch.uint8)
             dist.all_gather_into_tensor(host, send.cpu(), group=group)
             recv.copy_(host)
         else:
             dist.all_gather_into_tensor(recv, send, group=group)
-        nodes = recv.view(world * widest, dlen).index_select(0, rows).view(-1)
+        torch.index_select(recv.view(world * widest, dlen), 0, rows, out=nodes2d)
+        nodes = nodes2d.view(-1)
+        if shard_plan.n_shards == 1:
+            return nodes
     else:
         widest = max(shard_plan.shard_count(r) for r in range(world))
         send = torch.zeros(widest * dlen, dtype=torch.uint8, device=backend.device)
@@ -178,6 +202,8 @@ def sharded_merkle_root(backend, shard_plan: ShardPlan, rank: int, world: int, g
             dist.all_gather_into_tensor(recv, send, group=group)
         parts = [recv[r * widest * dlen:(r * widest + shard_plan.shard_count(r)) * dlen] for r in range(world)]
         nodes = torch.cat(parts)
+        if shard_plan.n_shards == 1:
+            return nodes
     return backend.root_of(nodes, shard_plan.n_shards)
 
 
@@ -248,34 +274,19 @@ def sample_ranges(n_samples: int, world: int) -> List[Tuple[int, int]]:
     return ranges + [(n_samples, n_samples)] * (world - len(ranges))
 
 
-def allreduce_lattice(acc: torch.Tensor, counts: torch.Tensor, status: Optional[torch.Tensor] = None,
-                      group=None) -> None:
-    """Sum the widened lane accumulators and counts over all ranks, in place, with ONE all-reduce.
+def allreduce_lattice(state: torch.Tensor, group=None) -> None:
+    """Sum the per-rank LtHash accumulators over all ranks, in place, with ONE all-reduce.
 
-    ``acc`` is int32 (the bit pattern of u32 lanes), ``counts`` int64, ``status`` an int32 flag word.
-    The three are packed into one int64 buffer -- lanes zero-extended, the status flag as 0/1 -- so a
-    single ``all_reduce(SUM)`` of ``n_sources * 33 + STATUS_BITS`` words carries everything (a lane sum modulo
-    2^64 truncated to 32 bits is the sum modulo 2^32, hence still exact modulo 2^16; a summed flag is
-    non-zero exactly when some rank raised it; each of the STATUS_BITS flag bits travels as its own
-    word so the result is the OR of the ranks' flag words). The message is a few KB: latency bound, which is why
-    it is one collective and not three.
+    ``state`` is ``LatticeAccumulator.state``: lanes, counts and the status word in one int64 array
+    (the bit patterns of u64 sums). A lane sum modulo 2^64 is still exact modulo 2^16, counts add,
+    and a summed status word is non-zero exactly when some rank skipped a sample -- so one
+    ``all_reduce(SUM)`` of ``n_sources * 33 + 1`` words carries everything and there is nothing to
+    pack or unpack around it. The message is a few KB: latency bound, which is why it is one
+    collective and not three.
     """
-    n_acc, n_cnt = acc.numel(), counts.numel()
-    packed = torch.zeros(n_acc + n_cnt + STATUS_BITS, dtype=torch.int64, device=acc.device)
-    packed[:n_acc] = acc.to(torch.int64) & 0xFFFFFFFF
-    packed[n_acc:n_acc + n_cnt] = counts
-    if status is not None:
-        bits = torch.arange(STATUS_BITS, device=acc.device, dtype=torch.int64)
-        packed[n_acc + n_cnt:] = (status.reshape(-1)[:1].to(torch.int64) >> bits) & 1
-    if _needs_host_staging(packed, group):
-        host = packed.cpu()
+    if _needs_host_staging(state, group):           # debugging over gloo with ranks sharing a GPU
+        host = state.cpu()
         dist.all_reduce(host, op=dist.ReduceOp.SUM, group=group)
-        packed.copy_(host)
+        state.copy_(host)
     else:
-        dist.all_reduce(packed, op=dist.ReduceOp.SUM, group=group)
-    low = packed[:n_acc] & 0xFFFFFFFF
-    acc.copy_((((low + 0x80000000) & 0xFFFFFFFF) - 0x80000000).to(torch.int32))   # u32 bit pattern as int32
-    counts.copy_(packed[n_acc:n_acc + n_cnt])
-    if status is not None:
-        bits = torch.arange(STATUS_BITS, device=acc.device, dtype=torch.int64)
-        status.copy_((((packed[n_acc + n_cnt:] != 0).to(torch.int64) << bits).sum()).to(status.dtype).reshape(1))
+        dist.all_reduce(state, op=dist.ReduceOp.SUM, group=group)

@@ -92,22 +92,24 @@ def _lattice_worker(rank, world, port, q):
         samples = inputs.dataset_samples(**spec)
         sources = sorted(spec["declared"])
         a, b = dd.sample_ranges(len(samples), world)[rank]
-        # per-rank partial sums in the widened u32 layout the kernels use
-        acc = np.zeros((len(sources), 32), dtype=np.uint32)
-        counts = np.zeros(len(sources), dtype=np.int64)
+        # per-rank partial sums in the layout LatticeAccumulator.state has: lanes | counts | status, all u64
+        n_src = len(sources)
+        state = np.zeros(n_src * 33 + 1, dtype=np.uint64)
+        acc, counts = state[:n_src * 32].reshape(n_src, 32), state[n_src * 32:n_src * 33]
         for sid, src, _label, data in samples[a:b]:
-            lanes = np.frombuffer(orc.sample_digest(sid, data), dtype="<u2").astype(np.uint32)
+            lanes = np.frombuffer(orc.sample_digest(sid, data), dtype="<u2").astype(np.uint64)
             acc[sources.index(src)] += lanes
             counts[sources.index(src)] += 1
-        acc[0, 0] += np.uint32(0xFFFF0000)          # force a wrap modulo 2^32 in the all-reduce on one lane
-        t_acc = torch.from_numpy(acc.view(np.int32).reshape(-1).copy())
-        t_cnt = torch.from_numpy(counts.copy())
-        t_status = torch.tensor([1 if rank == 1 else 4], dtype=torch.int32)   # flag words are OR-ed
-        dd.allreduce_lattice(t_acc, t_cnt, t_status)
-        assert int(t_status.item()) == 5
-        got = (t_acc.numpy().view(np.uint32).reshape(len(sources), 32) & 0xFFFF).astype("<u2")
+        acc[0, 0] += np.uint64(0xFFFFFFFFFFFF0000)  # force a wrap modulo 2^64 in the all-reduce on one lane
+        state[-1] = 2 if rank == 1 else 0           # rank 1 skipped two samples of an undeclared source
+        t_state = torch.from_numpy(state.view(np.int64).copy())
+        dd.allreduce_lattice(t_state)
+        summed = t_state.numpy().view(np.uint64)
+        assert int(summed[-1]) == 2
+        got = (summed[:n_src * 32].reshape(n_src, 32) & np.uint64(0xFFFF)).astype("<u2")
         want = orc.dataset_digests(samples, declared=sources)
-        ok = all(got[i].tobytes() == want[s][0] and int(t_cnt[i]) == want[s][1] for i, s in enumerate(sources))
+        ok = all(got[i].tobytes() == want[s][0] and int(summed[n_src * 32 + i]) == want[s][1]
+                 for i, s in enumerate(sources))
         q.put((rank, ok))
     finally:
         dist.destroy_process_group()

@@ -98,3 +98,95 @@ def test_ranks_sharing_the_gpu_reproduce_single_gpu_digests(world, porc):
         for alg in ("sha256", "blake2b", "sha3-256"):
             assert got[alg] == porc.inplace_merkle(alg, tensors, 8192).hex(), (rank, alg)
         assert got["lattice"] == {k: (v[0].hex(), v[1]) for k, v in want_lat.items()}, rank
+
+
+# ---- NCCL ---------------------------------------------------------------------------------------
+# The product's collectives are NCCL calls on device tensors. The test box has one GPU and NCCL refuses
+# two ranks on one device, so (a) a ONE-rank NCCL group runs the exact calls of the multi-GPU path
+# (all_gather_into_tensor of uint8 shard-root slots, one int64 all_reduce of the lattice state) with
+# ``always_gather`` forcing the exchange, and (b) a real two-rank test runs wherever two devices exist.
+
+def _nccl_worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    try:
+        torch.cuda.set_device(rank)
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
+        from paper_2510_00554_b200 import device as dev, distributed as dd
+
+        sizes = [8192 * 1500 + 77, 100, 0, 8192 * 2100, 31, 8192 * 900 + 4096, 5000]
+        tensors = inputs.model_tensors(91, sizes)
+        flat = [torch.frombuffer(bytearray(t), dtype=torch.uint8).cuda() if t else torch.empty(0, dtype=torch.uint8, device="cuda")
+                for t in tensors]
+        plan = dev.ModelPlan(flat, 8192)
+        out = {}
+        for alg in ("sha256", "blake2b", "sha3-256"):
+            backend = dd.CudaBackend(plan, alg)
+            sp = dd.plan_shards(plan.leaf_count, world)
+            roots = [dd.sharded_merkle_root(backend, sp, rank, world, always_gather=True) for _ in range(3)]
+            torch.cuda.synchronize()
+            out[alg] = backend.to_bytes(roots[-1]).hex()
+        n, n_src = 4000, 5
+        rng = np.random.default_rng(3)
+        data = torch.from_numpy(rng.integers(0, 256, size=(n, 200), dtype=np.uint8)).cuda()
+        ids = torch.arange(n, dtype=torch.int64)
+        src = torch.from_numpy(rng.integers(0, n_src, size=n))
+        from paper_2510_00554_b200 import dataset as dsm
+
+        a, b = dd.sample_ranges(n, world)[rank]
+        h = dsm.StreamingDatasetHasher(range(n_src))
+        h.update(data[a:b], ids[a:b], src[a:b])
+        h.allreduce()                                      # one NCCL all_reduce of the int64 state
+        out["lattice"] = {k: (v[0].data.hex(), v[1]) for k, v in h.finalize().items()}
+        q.put((rank, out))
+    except Exception as exc:
+        q.put((rank, {"error": repr(exc)}))
+        os._exit(1)
+    finally:
+        if dist.is_initialized():
+            dist.destroy_process_group()
+
+
+def _run_nccl(world, porc):
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_nccl_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = {}
+    try:
+        for _ in range(world):
+            rank, out = q.get(timeout=300)
+            assert "error" not in out, (rank, out)
+            results[rank] = out
+        for p in procs:
+            p.join(60)
+            assert p.exitcode == 0
+    finally:
+        for p in procs:
+            if p.is_alive():
+                p.kill()
+    sizes = [8192 * 1500 + 77, 100, 0, 8192 * 2100, 31, 8192 * 900 + 4096, 5000]
+    tensors = inputs.model_tensors(91, sizes)
+    n, n_src = 4000, 5
+    rng = np.random.default_rng(3)
+    data = rng.integers(0, 256, size=(n, 200), dtype=np.uint8)
+    src = rng.integers(0, n_src, size=n)
+    want_lat = porc.dataset_digests([(i, int(src[i]), b"", data[i].tobytes()) for i in range(n)], declared=range(n_src))
+    for rank in range(world):
+        for alg in ("sha256", "blake2b", "sha3-256"):
+            assert results[rank][alg] == porc.inplace_merkle(alg, tensors, 8192).hex(), (rank, alg)
+        assert results[rank]["lattice"] == {k: (v[0].hex(), v[1]) for k, v in want_lat.items()}, rank
+
+
+def test_nccl_collectives_of_the_shard_path_one_rank_group(porc):
+    _run_nccl(1, porc)
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs two CUDA devices (the test box has one)")
+def test_nccl_two_gpus_reproduce_single_gpu_digests(porc):
+    _run_nccl(2, porc)

@@ -162,3 +162,51 @@ def test_time_sliced_tail_is_exercised(dev, corc):
         assert leaves == want_leaves, alg
         assert root == corc.merkle_root(alg, want_leaves, plan.leaf_count, threads), alg
         assert launches == 1
+
+
+def test_lthash_chain_kernel_matches_grid_and_oracle(dev, corc):
+    """LtHash through the persistent chain kernel (time-sliced tail, parked BLAKE2b states) against the plain grid
+    and the C oracle: ragged samples, every alignment, more chains than warps per SM, > 128 sources (global
+    atomics), undeclared sources, per-sample digests."""
+    from paper_2510_00554_b200 import _native
+
+    lib = _native.load()
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    rng = np.random.default_rng(41)
+    for n, n_src, max_len in ((sms * 32 * 11 + 17, 16, 700), (5000, 200, 3000), (33, 3, 70000), (1, 1, 10)):
+        lens = rng.integers(0, max_len, size=n).astype(np.uint64)
+        if n > 100:
+            lens[::97] = 0                                   # empty samples
+            lens[5] = 4 * max_len                            # one chain much longer than its neighbours
+        offs = np.zeros(n, dtype=np.uint64)
+        np.cumsum(lens[:-1] + rng.integers(0, 3, size=n - 1).astype(np.uint64), out=offs[1:])   # gaps: odd addresses
+        shard = rng.integers(0, 256, size=int(offs[-1] + lens[-1]) + 16, dtype=np.uint8)
+        slots = rng.integers(0, n_src, size=n).astype(np.uint32)
+        bad = rng.choice(n, size=min(3, n - 1), replace=False) if n > 1 else np.array([], dtype=np.int64)
+        slots_bad = slots.copy()
+        slots_bad[bad] = n_src + 5                           # undeclared sources: skipped and counted
+        ids = rng.integers(0, 2**63, size=n).astype(np.uint64)
+        d_shard = torch.from_numpy(shard).cuda()
+        d_off, d_len, d_ids = (torch.from_numpy(a.view(np.int64)).cuda() for a in (offs, lens, ids))
+        keep = np.ones(n, dtype=bool)
+        keep[bad] = False
+        want_sums, want_counts, want_dig = corc.lthash_samples(shard, offs[keep], lens[keep], ids[keep], slots[keep], n_src,
+                                                              4, want_digests=True)
+        results = {}
+        try:
+            for schedule in (_native.SCHEDULE_FUSED, _native.SCHEDULE_PERSISTENT, _native.SCHEDULE_GRID):   # chains forced, auto, grid
+                lib.snt_merkle_schedule(schedule)
+                acc = dev.LatticeAccumulator(n_src)
+                dig = torch.zeros(n * 64, dtype=torch.uint8, device="cuda")
+                acc.add_samples(d_shard, d_off, d_len, d_ids, torch.from_numpy(slots_bad.view(np.int32)).cuda(), dig)
+                acc.add_samples(d_shard, d_off, d_len, d_ids, torch.from_numpy(slots_bad.view(np.int32)).cuda(), dig)
+                out, counts, status = acc.digests()
+                results[schedule] = (out, counts, status, dig.cpu().numpy().reshape(n, 64)[keep].tobytes())
+        finally:
+            lib.snt_merkle_schedule(_native.SCHEDULE_PERSISTENT)
+        for schedule, (out, counts, status, dig) in results.items():
+            assert status == 2 * len(bad), (n, schedule)
+            assert counts == [2 * c for c in want_counts], (n, schedule)
+            doubled = ((np.frombuffer(want_sums, dtype="<u2").astype(np.uint32) * 2) & 0xFFFF).astype("<u2").tobytes()
+            assert out == doubled, (n, schedule)
+            assert dig == want_dig, (n, schedule)

@@ -313,3 +313,32 @@ def test_verdict_classes_and_precedence(tmp_path):
         pkg.canonicalize(pkg.Statement([], "t", {}))
     with pytest.raises(FormatError):
         pkg.canonicalize(pkg.Statement([pkg.Subject("s", {"sha256": "abcd"})], "t", {}))
+
+
+def test_block_size_above_the_abi_range_is_a_config_error():
+    """A block size the uint32 ABI parameter cannot carry is refused before anything is allocated."""
+    import paper_2510_00554_b200 as pkg
+
+    for bs in (1 << 32, 1 << 40):
+        cfg = pkg.HashConfig(pkg.Construction.MERKLE, pkg.Strategy.COALESCED, pkg.CompressionAlg.SHA256, bs)
+        with pytest.raises(pkg.errors.ConfigError):
+            cfg.validate()
+        with pytest.raises(pkg.errors.ConfigError):
+            pkg.hash_model(cfg, pkg.TensorMap([("a", b"x" * 10)]))
+        pred = dict(cfg.predicate())
+        with pytest.raises(pkg.errors.ConfigError):
+            pkg.HashConfig.from_predicate(pred)
+    pkg.HashConfig(pkg.Construction.MERKLE, pkg.Strategy.IN_PLACE, pkg.CompressionAlg.SHA256, 1 << 31).validate()
+
+
+def test_sample_ids_outside_u64_are_rejected_not_wrapped():
+    import paper_2510_00554_b200 as pkg
+    from paper_2510_00554_b200 import dataset as dsm
+
+    for bad in (-1, 1 << 64):
+        with pytest.raises(pkg.errors.ValidationError):
+            dsm._checked_ids([0, bad])
+        acc = pkg.SourceAccumulator()
+        with pytest.raises(pkg.errors.ValidationError):          # raised before anything touches the device
+            pkg.process_batch(pkg.Batch([pkg.SampleRecord(bad, 0, b"", b"data")]), acc)
+    assert dsm._checked_ids([0, (1 << 64) - 1]).dtype.name == "uint64"

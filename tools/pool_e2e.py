@@ -93,7 +93,7 @@ def main():
         if world > 1:
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            dd.allreduce_lattice(acc.acc, acc.counts, acc.status)
+            dd.allreduce_lattice(acc.state)
             torch.cuda.synchronize()
             t_coll = time.perf_counter() - t0
         out, counts, status = acc.digests()
