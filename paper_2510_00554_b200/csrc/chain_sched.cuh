@@ -6,6 +6,14 @@
 // the chain (state in shared memory, progress in `prog`) at the tail of the FIFO and takes the chain at
 // its head, so that all W warps -- W/4 on every scheduler -- stay busy until the SM's work is done and
 // the SM finishes after count/W chain-times instead of ceil(count/W).
+//
+// Synchronisation is a spin lock in shared memory taken by lane 0 of a warp (no warp ever waits for
+// another except for the few instructions inside the lock) plus fences: a parking warp writes the state
+// (all lanes), __threadfence_block + __syncwarp, then lane 0 publishes the chain under the lock; a resuming
+// warp's lane 0 takes the chain under the lock, and __syncwarp orders that before the other lanes' reads.
+// compute-sanitizer's racecheck models barriers only and therefore reports these lock-ordered accesses
+// (fresh / head / tail / ring / prog and the parked states) as hazards; memcheck and synccheck are clean
+// and every result is checked against hashlib (tools/sanitize_smoke.py).
 #pragma once
 #include "common.cuh"
 
@@ -43,7 +51,9 @@ SNT_D int sched_pop(FusedSched* sc, int count, int lane) {
         else if (sc->head != sc->tail) ch = sc->ring[(sc->head++) & (FUSED_RING - 1)];
         sched_unlock(sc);
     }
-    return __shfl_sync(0xffffffffu, ch, 0);
+    ch = __shfl_sync(0xffffffffu, ch, 0);
+    __syncwarp();       // orders lane 0's acquire before the other lanes' reads of the chain's parked state
+    return ch;
 }
 
 // Is any chain waiting for a warp? (A warp that finishes a slice keeps its chain when nobody is.)
