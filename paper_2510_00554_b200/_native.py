@@ -39,6 +39,7 @@ SIGNATURES = {
     "snt_debug_fused_trace": (None, [c_void_p]),
     "snt_merkle_work_bytes": (c_size_t, [c_int, c_uint64]),
     "snt_merkle_work_init": (c_int, [c_void_p, c_size_t, c_void_p]),
+    "snt_memcpy_h2d_batch": (c_int, [c_void_p, c_void_p, c_void_p, c_uint32, c_void_p]),
     "snt_gather_chunk_bytes": (c_uint32, []),
     "snt_gather_spans": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_uint32, c_uint64, c_uint32, c_void_p,
                                  c_void_p]),

@@ -723,6 +723,18 @@ int snt_merkle_roots_segmented(int alg, const void* d_digests, const uint64_t* s
     return SNT_OK;
 }
 
+int snt_memcpy_h2d_batch(void* const* d_dst, const void* const* h_src, const uint64_t* nbytes, uint32_t n,
+                         snt_stream_t stream) {
+    if (n && (!d_dst || !h_src || !nbytes)) return SNT_ERR_INVALID_INPUT;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    for (uint32_t i = 0; i < n; ++i) {
+        if (!nbytes[i]) continue;
+        if (!d_dst[i] || !h_src[i]) return SNT_ERR_INVALID_INPUT;
+        SNT_CUDA(cudaMemcpyAsync(d_dst[i], h_src[i], nbytes[i], cudaMemcpyHostToDevice, s));
+    }
+    return SNT_OK;
+}
+
 uint32_t snt_gather_chunk_bytes(void) { return GATHER_CHUNK_BYTES; }
 
 int snt_gather_spans(const uint64_t* d_src_addr, const uint64_t* d_len, const uint64_t* d_dst_off,
