@@ -288,7 +288,7 @@ def _inplace_merkle_pinned(cfg: HashConfig, model: TensorMap) -> Optional[ModelD
                     b = batches[turn]
                     b[0].append(int(ptrs[i])); b[1].append(host_ptrs[i]); b[2].append(nbytes)
                     if nbytes >= (1 << 20):
-                        turn ^= 1
+                        turn = (turn + 1) % len(sides)
             group_bytes += nbytes
             first += -(-nbytes // bs)
             if group_bytes >= STAGE_CHUNK_BYTES or i == n - 1:
