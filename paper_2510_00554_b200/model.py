@@ -468,11 +468,13 @@ def _inplace_merkle_staged(cfg: HashConfig, model: TensorMap, workers: int = 1) 
 class _ResidentEntry:
     """Plan + workspace of one device-resident model: what a repeated ``hash_model`` call re-uses."""
 
-    __slots__ = ("key", "tensors", "ids", "plan", "hasher", "host", "busy")
+    __slots__ = ("key", "storages", "ids", "plan", "hasher", "host", "busy")
 
     def __init__(self, key, tensors, plan, hasher, host):
         self.key = key                   # (ptrs, sizes, block size, algorithm, device, stream)
-        self.tensors = tensors           # the tensor objects the plan was built from: keeps their memory alive
+        # the STORAGES the plan's addresses point into (not the tensor objects, which can be re-pointed with
+        # `.data =` / `set_`): as long as the entry lives, a launch from the cached plan reads allocated memory
+        self.storages = [t.untyped_storage() for t in tensors]
         self.ids = tuple(map(id, tensors))
         self.plan, self.hasher, self.host = plan, hasher, host
         self.busy = threading.Lock()     # one call at a time owns the workspace
@@ -507,7 +509,7 @@ def _inplace_merkle_resident(cfg: HashConfig, model: TensorMap, buffers) -> Mode
     The plan (device block table), the leaf-digest buffer, the reducer workspace and a pinned root buffer
     hang off the ``TensorMap`` itself, so they live exactly as long as the model the caller holds. When the
     same ``TensorMap`` (same tensor objects) is hashed again the kernels are launched FIRST, from the cached
-    plan -- its tensors are kept alive by the entry, so the addresses are valid memory whatever happened --
+    plan -- the entry holds the storages behind its addresses, so they are allocated memory whatever happened --
     and the per-tensor checks (address, length, contiguity: ~0.4 us per tensor in Python) run while the GPU
     works. Only if a check fails (a tensor was re-pointed or resized in place) is the result thrown away
     and the model hashed again through a fresh plan. Nothing unchecked is ever returned.

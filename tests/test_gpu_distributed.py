@@ -1,7 +1,11 @@
-"""The multi-rank shard-and-combine path on real CUDA kernels: several ranks share the one GPU of
-the test box and talk over gloo (NCCL refuses two ranks on one device). Everything but the NCCL
-call itself is the product path: per-rank leaf ranges, shard roots written into the all-gather
-slot, index-compacted receive buffer, top reduce; packed lattice all-reduce.
+"""The multi-rank shard-and-combine path on real CUDA kernels.
+
+* Several ranks share the one GPU of the test box and talk over gloo (NCCL refuses two ranks on one device):
+  everything but the NCCL call itself is the product path -- per-rank leaf ranges, shard roots written into the
+  all-gather slot, index-compacted receive buffer, top reduce; one all-reduce of the lattice state.
+* A one-rank NCCL group runs the exact NCCL calls of that path on the device (uint8 all_gather_into_tensor of
+  shard-root slots, int64 all_reduce of the lattice state).
+* A two-rank NCCL test runs wherever two devices exist (skipped on the one-GPU box).
 """
 
 import os

@@ -210,3 +210,83 @@ def test_lthash_chain_kernel_matches_grid_and_oracle(dev, corc):
             doubled = ((np.frombuffer(want_sums, dtype="<u2").astype(np.uint32) * 2) & 0xFFFF).astype("<u2").tobytes()
             assert out == doubled, (n, schedule)
             assert dig == want_dig, (n, schedule)
+
+
+def test_resident_model_cache_revalidates_every_call(porc):
+    """hash_model on a TensorMap of CUDA tensors re-uses plan and workspace, launches before it re-checks the tensors,
+    and still never returns a digest for bytes it did not check: content changes, re-pointed tensors, resized tensors
+    and replaced entries all give the oracle's answer; a second TensorMap over the same tensors gets its own entry."""
+    import paper_2510_00554_b200 as pkg
+    from paper_2510_00554_b200 import model as mm
+
+    rng = np.random.default_rng(3)
+    sizes = [8192 * 50 + 100, 4096, 8192 * 300, 12, 8192 * 7]
+    host = [rng.integers(0, 256, size=s, dtype=np.uint8) for s in sizes]
+    tensors = [torch.from_numpy(h).cuda() for h in host]
+    model = pkg.TensorMap([(f"t{i}", t) for i, t in enumerate(tensors)])
+
+    def want(alg):
+        return porc.inplace_merkle(alg, [h.tobytes() for h in host], 8192)
+
+    for alg in ("sha256", "blake2b"):
+        cfg = pkg.HashConfig(pkg.Construction.MERKLE, pkg.Strategy.IN_PLACE, pkg.CompressionAlg.from_name(alg))
+        assert pkg.hash_model(cfg, model).model_digest.data == want(alg)
+        assert "_resident" in model.__dict__
+        entry = model.__dict__["_resident"]
+        assert pkg.hash_model(cfg, model).model_digest.data == want(alg)
+        assert model.__dict__["_resident"] is entry                      # re-used
+        # 1. content changes in place: same plan, new digest
+        host[2][12345] ^= 0xFF
+        tensors[2][12345] ^= 0xFF
+        assert pkg.hash_model(cfg, model).model_digest.data == want(alg)
+        assert model.__dict__["_resident"] is entry
+        # 2. a tensor object re-pointed to other storage (same id, other address): speculation is discarded
+        host[1] = rng.integers(0, 256, size=4096, dtype=np.uint8)
+        tensors[1].data = torch.from_numpy(host[1]).cuda()
+        assert pkg.hash_model(cfg, model).model_digest.data == want(alg)
+        assert model.__dict__["_resident"] is not entry
+        entry = model.__dict__["_resident"]
+        # 3. an entry replaced by a tensor of another size
+        host[3] = rng.integers(0, 256, size=9000, dtype=np.uint8)
+        tensors[3] = torch.from_numpy(host[3]).cuda()
+        model.entries[3] = ("t3", tensors[3])
+        assert pkg.hash_model(cfg, model).model_digest.data == want(alg)
+        # 4. a non-contiguous view falls back to the uncached path and hashes the logical bytes
+        base = torch.from_numpy(rng.integers(0, 256, size=(64, 256), dtype=np.uint8)).cuda()
+        view = base.t()
+        m2 = pkg.TensorMap([("v", view), ("w", tensors[0])])
+        assert pkg.hash_model(cfg, m2).model_digest.data == \
+            porc.inplace_merkle(alg, [view.contiguous().cpu().numpy().tobytes(), host[0].tobytes()], 8192)
+        # 5. another TensorMap over the same tensors: its own entry, same digest
+        m3 = pkg.TensorMap([(f"t{i}", t) for i, t in enumerate(tensors)])
+        assert pkg.hash_model(cfg, m3).model_digest.data == want(alg)
+        assert m3.__dict__["_resident"] is not model.__dict__["_resident"]
+        mm.clear_hash_cache(model)
+        assert "_resident" not in model.__dict__
+        assert pkg.hash_model(cfg, model).model_digest.data == want(alg)
+
+
+def test_process_batch_keeps_sums_on_the_device(porc):
+    """The reference's loader protocol on the device-resident accumulator: many small batches, sources appearing late
+    (slot table growth past its first capacity), cover_labels, reads of acc.sums in the middle, merge of two accumulators."""
+    import paper_2510_00554_b200 as pkg
+
+    rng = np.random.default_rng(9)
+    n, n_src = 3000, 70                                   # more sources than the engine's first 32 slots
+    samples = []
+    for i in range(n):
+        src = int(rng.integers(0, 1 + min(n_src - 1, i // 20)))          # later sources show up as the loop goes on
+        data = rng.integers(0, 256, size=int(rng.integers(0, 400)), dtype=np.uint8).tobytes()
+        samples.append((10_000 + i, src, f"c{i % 5}".encode(), data))
+    for cover in (False, True):
+        acc = pkg.SourceAccumulator(cover_labels=cover)
+        other = pkg.SourceAccumulator(cover_labels=cover)
+        for s in range(0, n, 37):
+            recs = [pkg.SampleRecord(*t) for t in samples[s:s + 37]]
+            pkg.process_batch(pkg.Batch(recs), acc if (s // 37) % 3 else other)
+            if s == 37 * 20:
+                assert sum(acc.counts.values()) + sum(other.counts.values()) == s + len(recs)    # mid-stream read
+        acc.merge(other)
+        got = pkg.finalize(acc)
+        want = porc.dataset_digests(samples, cover_labels=cover)
+        assert {k: (v[0].data, v[1]) for k, v in got.items()} == {k: (v[0], v[1]) for k, v in want.items()}
