@@ -489,7 +489,7 @@ def _resident_key(buffers, cfg: HashConfig, stream):
     n = len(buffers)
     ptrs = np.fromiter((b.data_ptr() for b in buffers), dtype=np.uint64, count=n)
     sizes = np.fromiter((b.nbytes for b in buffers), dtype=np.uint64, count=n)
-    contiguous = all(b.is_contiguous() for b in buffers)
+    contiguous = all(b.is_cuda and b.is_contiguous() for b in buffers)   # `.data = cpu_tensor` moves a tensor object
     ptrs[sizes == 0] = 0
     return (ptrs.tobytes(), sizes.tobytes(), cfg.block_size, cfg.alg.value, stream.device_index, stream.cuda_stream), \
         ptrs, sizes, contiguous
@@ -503,7 +503,7 @@ def clear_hash_cache(model: Optional[TensorMap] = None) -> None:
             entry.close()
 
 
-def _inplace_merkle_resident(cfg: HashConfig, model: TensorMap, buffers) -> ModelDigestResult:
+def _inplace_merkle_resident(cfg: HashConfig, model: TensorMap, buffers, same_objects=None) -> ModelDigestResult:
     """Every tensor already lives in HBM: hash in place, re-using the plan and workspace of the last call.
 
     The plan (device block table), the leaf-digest buffer, the reducer workspace and a pinned root buffer
@@ -517,7 +517,7 @@ def _inplace_merkle_resident(cfg: HashConfig, model: TensorMap, buffers) -> Mode
     stream = torch.cuda.current_stream()
     entry: Optional[_ResidentEntry] = model.__dict__.get("_resident")
     launched = False
-    if entry is not None and entry.ids == tuple(map(id, buffers)) and entry.key[2:] == \
+    if entry is not None and (entry is same_objects or entry.ids == tuple(map(id, buffers))) and entry.key[2:] == \
             (cfg.block_size, cfg.alg.value, stream.device_index, stream.cuda_stream) and entry.busy.acquire(blocking=False):
         entry.hasher.run()                                   # speculative: validated below, before anything is returned
         entry.host.copy_(entry.hasher.out, non_blocking=True)
@@ -528,6 +528,9 @@ def _inplace_merkle_resident(cfg: HashConfig, model: TensorMap, buffers) -> Mode
         entry.busy.release()
         launched = False
     if not launched:
+        if not all(b.is_cuda for b in buffers):              # a cached tensor object was moved to the host in place
+            clear_hash_cache(model)
+            return inplace_hash(cfg, model)
         if entry is not None and entry.busy.locked():        # another thread is hashing this very TensorMap: do not share
             return _inplace_merkle_uncached(cfg, buffers)
         if not contiguous:
@@ -568,6 +571,9 @@ def _inplace_merkle_uncached(cfg: HashConfig, buffers) -> ModelDigestResult:
 def inplace_hash(cfg: HashConfig, model: TensorMap, workers: int = 1) -> ModelDigestResult:
     """Hash fragmented tensors where they lie: no copy, no padding (model.py:298-315)."""
     buffers = [buf for _, buf in model.entries]
+    cached = model.__dict__.get("_resident")
+    if cached is not None and cfg.construction is Construction.MERKLE and cached.ids == tuple(map(id, buffers)):
+        return _inplace_merkle_resident(cfg, model, buffers, same_objects=cached)   # launch first, re-check after
     all_resident = all(type(buf) is torch.Tensor and buf.is_cuda for buf in buffers)
     if all_resident and buffers and cfg.construction is Construction.MERKLE:
         return _inplace_merkle_resident(cfg, model, buffers)

@@ -261,6 +261,13 @@ def test_resident_model_cache_revalidates_every_call(porc):
         m3 = pkg.TensorMap([(f"t{i}", t) for i, t in enumerate(tensors)])
         assert pkg.hash_model(cfg, m3).model_digest.data == want(alg)
         assert m3.__dict__["_resident"] is not model.__dict__["_resident"]
+        # 6. a cached tensor object moved to the host in place (same id, no longer a CUDA tensor): generic path
+        assert pkg.hash_model(cfg, m3).model_digest.data == want(alg)
+        host[4] = rng.integers(0, 256, size=sizes[4], dtype=np.uint8)
+        tensors[4].data = torch.from_numpy(host[4])
+        assert pkg.hash_model(cfg, m3).model_digest.data == want(alg)
+        assert "_resident" not in m3.__dict__
+        tensors[4].data = torch.from_numpy(host[4]).cuda()
         mm.clear_hash_cache(model)
         assert "_resident" not in model.__dict__
         assert pkg.hash_model(cfg, model).model_digest.data == want(alg)
