@@ -343,6 +343,20 @@ def gpu_model_config(pkg, dev, shapes, arch, alg, device, steps, hbm_peak, peak_
            "root": root,
            "roofline": model_roofline(alg, arch, leaf_ms, plan.leaf_count, plan.total_bytes, step_ms, hbm_peak, peak_src,
                                       peaks, traffic_db.get(f"merkle_fused_kernel<{alg}>:{arch}"))}
+    # the public call on the same resident tensors: host wall clock per hash_model(cfg, TensorMap(CUDA tensors))
+    api_cfg = pkg.HashConfig(pkg.Construction.MERKLE, pkg.Strategy.IN_PLACE, pkg.CompressionAlg.from_name(alg))
+    model_r = pkg.TensorMap([(name, t) for name, t in sd])
+    for _ in range(3):
+        got_r = pkg.hash_model(api_cfg, model_r).model_digest.data
+    assert got_r.hex() == root, f"{arch}/{alg}: hash_model on resident tensors differs from the planned hasher"
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        pkg.hash_model(api_cfg, model_r)
+    dt_r = (time.perf_counter() - t0) / steps
+    out["api_device_resident"] = {"ms_per_call": round(dt_r * 1e3, 4),
+                                  "overhead_vs_value_pct": round((dt_r * 1e3 / step_ms - 1) * 100, 2)}
+    del model_r
     if ref is not None:
         host = host_views(sd)
         cfg = reference_cfg(ref, alg)
@@ -607,8 +621,9 @@ def run_ours(args):
         int_pipe = {"alu_pipe_utilisation": roofline.get("binding_unit_frac"),
                     "issue_budget_frac": roofline.get("issue_budget_frac"),
                     "model_ops_tops": round(SHA256_OPS_PER_LEAF * my_leaves / (leaf_ms * 1e-3) / 1e12, 3),
-                    "compute_only_gbs": ceiling,
-                    "frac_of_compute_only": round(roofline["achieved"] / ceiling, 4) if ceiling else None,
+                    # the register-only loop of tools/intpeak (same compression, no loads, plain grid): a reference
+                    # point, not a bound -- the persistent kernel's scheduling beats it, so no fraction is formed
+                    "register_only_loop_gbs": ceiling,
                     "ops_model": "model_ops_tops counts SURVEY.md 8(d)'s 180,600 abstract 32-bit ops per leaf; the kernel "
                                  "issues them as ALU-pipe and FMA-pipe (IMAD) instructions, so utilisation is stated per "
                                  "pipe and against the combined issue budget, never above 1",

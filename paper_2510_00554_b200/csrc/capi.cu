@@ -572,7 +572,7 @@ int snt_merkle_inplace(const snt_model_plan* plan, int alg, uint64_t leaf_begin,
     const uint32_t dlen = snt_digest_len(alg);
     if (levels == 0) {
         SNT_CUDA(cudaMemcpyAsync(d_out, leaves, static_cast<size_t>(leaf_end - leaf_begin) * dlen,
-                                 cudaMemcpyDeviceToDevice, s));
+                                 cudaMemcpyDefault, s));
         return SNT_OK;
     }
     return reduce_chain(alg, leaves, leaf_begin, leaf_end - leaf_begin, n, levels,
@@ -614,7 +614,7 @@ int snt_merkle_root(int alg, const void* d_nodes, uint64_t count, void* d_work, 
     if (count == 0 || !d_nodes || !d_root) return SNT_ERR_INVALID_INPUT;              // merkle.py:156-157
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     if (count == 1) {                                                                 // merkle.py:159-160
-        SNT_CUDA(cudaMemcpyAsync(d_root, d_nodes, snt_digest_len(alg), cudaMemcpyDeviceToDevice, s));
+        SNT_CUDA(cudaMemcpyAsync(d_root, d_nodes, snt_digest_len(alg), cudaMemcpyDefault, s));
         return SNT_OK;
     }
     return reduce_chain(alg, static_cast<const uint8_t*>(d_nodes), 0, count, count, ceil_log2(count),

@@ -388,9 +388,11 @@ class MerkleModelHasher:
     """
 
     def __init__(self, plan: ModelPlan, alg: str, leaf_begin: int = 0, leaf_end: Optional[int] = None,
-                 levels: Optional[int] = None, out_capacity: Optional[int] = None):
+                 levels: Optional[int] = None, out_capacity: Optional[int] = None, host_out: bool = False):
         """``out_capacity`` (in digests) over-allocates the zero-filled output buffer so that a rank's
-        shard roots can be handed to an all-gather of fixed-size slots without a staging copy."""
+        shard roots can be handed to an all-gather of fixed-size slots without a staging copy.
+        ``host_out`` puts the output nodes in page-locked HOST memory: the last kernel of the hash stores the
+        root through the unified address space, so reading it needs a stream synchronisation and no copy."""
         self.plan = plan
         self.alg = alg
         self.dlen = DIGEST_LEN[alg]
@@ -407,7 +409,11 @@ class MerkleModelHasher:
         self.work_bytes = merkle_work_bytes(alg, count)
         # zeroed once: the fused kernel keeps its completion counters at zero between launches
         self.work = torch.zeros(max(self.work_bytes, 16), dtype=torch.uint8, device=dev)
-        self.out_padded = torch.zeros(max(self.n_out, out_capacity or 0) * self.dlen, dtype=torch.uint8, device=dev)
+        n_out_bytes = max(self.n_out, out_capacity or 0) * self.dlen
+        if host_out:
+            self.out_padded = torch.zeros(n_out_bytes, dtype=torch.uint8, pin_memory=True)
+        else:
+            self.out_padded = torch.zeros(n_out_bytes, dtype=torch.uint8, device=dev)
         self.out = self.out_padded[:self.n_out * self.dlen]
 
     def run(self) -> None:

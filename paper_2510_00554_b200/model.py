@@ -499,11 +499,15 @@ def clear_hash_cache(model: Optional[TensorMap] = None) -> None:
     """Release the plan / workspace a ``TensorMap`` of device tensors carries after it has been hashed."""
     if model is not None:
         entry = model.__dict__.pop("_resident", None)
-        if entry is not None:
-            entry.close()
+        # a thread that is hashing through this entry right now keeps it alive; its plan then goes with the entry
+        if entry is not None and entry.busy.acquire(blocking=False):
+            try:
+                entry.close()
+            finally:
+                entry.busy.release()
 
 
-def _inplace_merkle_resident(cfg: HashConfig, model: TensorMap, buffers, same_objects=None) -> ModelDigestResult:
+def _inplace_merkle_resident(cfg: HashConfig, model: TensorMap, buffers=None) -> ModelDigestResult:
     """Every tensor already lives in HBM: hash in place, re-using the plan and workspace of the last call.
 
     The plan (device block table), the leaf-digest buffer, the reducer workspace and a pinned root buffer
@@ -517,18 +521,25 @@ def _inplace_merkle_resident(cfg: HashConfig, model: TensorMap, buffers, same_ob
     stream = torch.cuda.current_stream()
     entry: Optional[_ResidentEntry] = model.__dict__.get("_resident")
     launched = False
-    if entry is not None and (entry is same_objects or entry.ids == tuple(map(id, buffers))) and entry.key[2:] == \
-            (cfg.block_size, cfg.alg.value, stream.device_index, stream.cuda_stream) and entry.busy.acquire(blocking=False):
-        entry.hasher.run()                                   # speculative: validated below, before anything is returned
-        entry.host.copy_(entry.hasher.out, non_blocking=True)
+    # O(1) checks only before the launch: the entry owns the storages its plan points into, so the speculative
+    # launch is safe whatever the caller did to the TensorMap; WHICH tensors it holds now is checked afterwards
+    if entry is not None and entry.key[2:] == (cfg.block_size, cfg.alg.value, stream.device_index, stream.cuda_stream) \
+            and entry.busy.acquire(blocking=False):
+        entry.hasher.run()                                   # root lands in pinned host memory (host_out)
         launched = True
-    key, ptrs, sizes, contiguous = _resident_key(buffers, cfg, stream)
-    if launched and (key != entry.key or not contiguous):
+    if buffers is None:
+        buffers = [buf for _, buf in model.entries]
+    if all(type(b) is torch.Tensor for b in buffers):
+        key, ptrs, sizes, contiguous = _resident_key(buffers, cfg, stream)
+        on_device = contiguous or all(b.is_cuda for b in buffers)
+    else:
+        key, contiguous, on_device = None, False, False
+    if launched and (key != entry.key or not contiguous or entry.ids != tuple(map(id, buffers))):
         stream.synchronize()
         entry.busy.release()
         launched = False
     if not launched:
-        if not all(b.is_cuda for b in buffers):              # a cached tensor object was moved to the host in place
+        if not on_device:                                    # the TensorMap no longer holds only device tensors
             clear_hash_cache(model)
             return inplace_hash(cfg, model)
         if entry is not None and entry.busy.locked():        # another thread is hashing this very TensorMap: do not share
@@ -537,18 +548,16 @@ def _inplace_merkle_resident(cfg: HashConfig, model: TensorMap, buffers, same_ob
             return _inplace_merkle_uncached(cfg, buffers)
         plan = _dev.ModelPlan.from_spans([], ptrs, sizes, cfg.block_size, count=len(buffers))   # rejects an empty model
         try:
-            hasher = _dev.MerkleModelHasher(plan, cfg.alg.value)
-            host = torch.empty(hasher.dlen, dtype=torch.uint8, pin_memory=True)
+            hasher = _dev.MerkleModelHasher(plan, cfg.alg.value, host_out=True)
         except Exception:
             plan.close()
             raise
-        old, entry = entry, _ResidentEntry(key, list(buffers), plan, hasher, host)
+        old, entry = entry, _ResidentEntry(key, list(buffers), plan, hasher, hasher.out)
         entry.busy.acquire()
         model.__dict__["_resident"] = entry
         if old is not None:
             old.close()
         entry.hasher.run()
-        entry.host.copy_(entry.hasher.out, non_blocking=True)
     try:
         stream.synchronize()
         root = Digest(cfg.alg, entry.host.numpy().tobytes())
@@ -570,10 +579,9 @@ def _inplace_merkle_uncached(cfg: HashConfig, buffers) -> ModelDigestResult:
 
 def inplace_hash(cfg: HashConfig, model: TensorMap, workers: int = 1) -> ModelDigestResult:
     """Hash fragmented tensors where they lie: no copy, no padding (model.py:298-315)."""
+    if cfg.construction is Construction.MERKLE and "_resident" in model.__dict__:
+        return _inplace_merkle_resident(cfg, model)          # launch first, re-check after
     buffers = [buf for _, buf in model.entries]
-    cached = model.__dict__.get("_resident")
-    if cached is not None and cfg.construction is Construction.MERKLE and cached.ids == tuple(map(id, buffers)):
-        return _inplace_merkle_resident(cfg, model, buffers, same_objects=cached)   # launch first, re-check after
     all_resident = all(type(buf) is torch.Tensor and buf.is_cuda for buf in buffers)
     if all_resident and buffers and cfg.construction is Construction.MERKLE:
         return _inplace_merkle_resident(cfg, model, buffers)
