@@ -472,7 +472,9 @@ def dataset_config(name, workload, arrays, np, torch, dsm, dev, dd, world, rank,
     my_bytes = int(lens[a:b].sum())
     blocks = int(((lens[a:b] + np.uint64(8 + 127)) // np.uint64(128)).sum())
     achieved = my_bytes / (kernel_ms * 1e-3) / 1e9
-    roof = {"bound": "hbm", "kernel": "lthash kernel (BLAKE2b per sample + per-source lane sums)", "achieved": round(achieved, 1),
+    kernel_name = ("lthash_kernel (one thread per sample: samples of one length)" if dset.uniform else
+                   "lthash_lanes_kernel (persistent lanes: ragged samples, no sort)")
+    roof = {"bound": "hbm", "kernel": kernel_name + ", BLAKE2b per sample + per-source lane sums", "achieved": round(achieved, 1),
             "peak": hbm_peak, "unit": "GB/s", "frac": round(achieved / hbm_peak, 4), "traffic": None, "peak_source": peak_src,
             "kernel_ms": round(kernel_ms, 4), "share_of_step": round(kernel_ms / ds_ms, 4), "algorithmic_bytes": my_bytes}
     if peaks and "error" not in peaks:

@@ -164,6 +164,16 @@ int snt_lthash_samples(const void* d_shard, const uint64_t* d_off, const uint64_
                        uint32_t n_sources, uint64_t* d_acc, uint64_t* d_counts, void* d_digests,
                        uint64_t* d_status, snt_stream_t stream);
 
+/* The same with what the caller knows about the sample lengths (it built d_len). Results never depend on
+ * it; the launch does: SNT_SAMPLES_UNKNOWN / _RAGGED take the persistent-lane kernel (every lane of a warp
+ * fetches its next sample the moment it finishes one, so ragged samples need no sorting), _UNIFORM -- all
+ * n lengths equal -- the one-thread-per-sample grid. snt_lthash_samples == shape SNT_SAMPLES_UNKNOWN. */
+typedef enum snt_samples_shape { SNT_SAMPLES_UNKNOWN = 0, SNT_SAMPLES_UNIFORM = 1, SNT_SAMPLES_RAGGED = 2 } snt_samples_shape;
+int snt_lthash_samples_shaped(const void* d_shard, const uint64_t* d_off, const uint64_t* d_len,
+                              const uint64_t* d_ids, const uint32_t* d_slot, uint64_t n,
+                              uint32_t n_sources, uint64_t* d_acc, uint64_t* d_counts, void* d_digests,
+                              uint64_t* d_status, uint32_t shape, snt_stream_t stream);
+
 /* inplace_hash, LATTICE construction (model.py:312-315): leaves
  * [leaf_begin, leaf_end) tagged LE64(k), summed into d_acc[32] / d_counts[1]. */
 int snt_lthash_model(const snt_model_plan* plan, uint64_t leaf_begin, uint64_t leaf_end,

@@ -21,7 +21,8 @@ LIB_PATH = Path(os.environ.get("SNT_LIB_PATH") or Path(__file__).resolve().paren
 
 SNT_LEVELS_TO_ROOT = 0xFFFFFFFF
 SCHEDULE_PERSISTENT, SCHEDULE_FUSED, SCHEDULE_GRID = 0, 1, 2
-ABI_VERSION = 2
+SAMPLES_UNKNOWN, SAMPLES_UNIFORM, SAMPLES_RAGGED = 0, 1, 2      # snt_samples_shape
+ABI_VERSION = 3
 
 # name -> (restype, argtypes); mirrors include/sentinel_b200.h one to one
 SIGNATURES = {
@@ -52,6 +53,8 @@ SIGNATURES = {
     "snt_merkle_root": (c_int, [c_int, c_void_p, c_uint64, c_void_p, c_size_t, c_void_p, c_void_p]),
     "snt_lthash_samples": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_uint64, c_uint32,
                                    c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "snt_lthash_samples_shaped": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_uint64, c_uint32,
+                                          c_void_p, c_void_p, c_void_p, c_void_p, c_uint32, c_void_p]),
     "snt_lthash_model": (c_int, [c_void_p, c_uint64, c_uint64, c_void_p, c_void_p, c_void_p, c_void_p]),
     "snt_lthash_model_layers": (c_int, [c_void_p, c_uint64, c_uint64, c_void_p, c_void_p, c_void_p, c_void_p]),
     "snt_merkle_roots_segmented": (c_int, [c_int, c_void_p, POINTER(c_uint64), c_uint32, c_void_p, c_void_p,

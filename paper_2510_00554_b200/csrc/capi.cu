@@ -14,6 +14,7 @@
 #include "../../include/sentinel_b200.h"
 #include "gather_kernels.cuh"
 #include "lthash_kernels.cuh"
+#include "lthash_lanes.cuh"
 #include "merkle_fused.cuh"
 #include "merkle_kernels.cuh"
 
@@ -168,7 +169,7 @@ const char* snt_strerror(int status) {
 
 const char* snt_last_cuda_error(void) { return g_cuda_err; }
 
-uint32_t snt_abi_version(void) { return 2; }
+uint32_t snt_abi_version(void) { return 3; }
 
 uint64_t snt_debug_launch_count(void) { return g_launches.load(); }
 
@@ -496,9 +497,34 @@ int launch_lthash_chains(const Items& items, uint64_t n, uint32_t n_sources, uns
     return SNT_OK;
 }
 
+// Persistent lanes (lthash_lanes.cuh): W warps per CTA, one CTA per SM, every warp a contiguous slice of the items.
+template <class Items, bool SMEM_ACC>
+int launch_lthash_lanes(const Items& items, uint64_t n, uint32_t n_sources, unsigned long long* acc,
+                        unsigned long long* counts, uint8_t* dig, unsigned long long* status, cudaStream_t s) {
+    constexpr size_t acc_max = LT_SMEM_SOURCES * (LT_LANES + 1) * sizeof(uint32_t);
+    static const cudaError_t attr = cudaFuncSetAttribute(
+        lthash_lanes_kernel<Items, SMEM_ACC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        static_cast<int>(LTL_MAXW * ltl_warp_bytes(Items::TAG_WORDS) + acc_max));
+    if (attr != cudaSuccess) return cuda_fail(attr, "cudaFuncSetAttribute(lthash_lanes_kernel)");
+    const uint64_t sms = static_cast<uint64_t>(sm_count());
+    // at least one item per lane, a multiple of four warps per CTA, at most three per scheduler
+    int warps = static_cast<int>((n / (sms * 32)) & ~3ull);
+    if (const char* force = getenv("SNT_LT_LANES_WARPS")) warps = atoi(force);
+    warps = warps < 4 ? 4 : (warps > LTL_MAXW ? LTL_MAXW : warps);
+    const uint64_t want_ctas = (n + static_cast<uint64_t>(warps) * 32 - 1) / (static_cast<uint64_t>(warps) * 32);
+    const unsigned grid = static_cast<unsigned>(want_ctas < sms ? want_ctas : sms);
+    const size_t smem = warps * ltl_warp_bytes(Items::TAG_WORDS) +
+                        (SMEM_ACC ? static_cast<size_t>(n_sources) * (LT_LANES + 1) * sizeof(uint32_t) : 0);
+    lthash_lanes_kernel<Items, SMEM_ACC><<<grid, warps * 32, smem, s>>>(items, n, n_sources, acc, counts, dig, status);
+    SNT_CUDA(cudaGetLastError());
+    ++g_launches;
+    return SNT_OK;
+}
+
 template <class Items>
 int launch_lthash(const Items& items, uint64_t n, uint32_t n_sources, uint64_t* d_acc,
-                  uint64_t* d_counts, void* d_digests, uint64_t* d_status, cudaStream_t s) {
+                  uint64_t* d_counts, void* d_digests, uint64_t* d_status, cudaStream_t s,
+                  uint32_t shape = SNT_SAMPLES_UNKNOWN) {
     if (n == 0) return SNT_OK;
     auto* counts = reinterpret_cast<unsigned long long*>(d_counts);
     auto* acc = reinterpret_cast<unsigned long long*>(d_acc);
@@ -516,6 +542,13 @@ int launch_lthash(const Items& items, uint64_t n, uint32_t n_sources, uint64_t* 
     if (schedule == SNT_SCHEDULE_FUSED || (Items::LONG_ITEMS && chains_per_sm < 32 && schedule != SNT_SCHEDULE_GRID)) {
         if (smem_acc) return launch_lthash_chains<Items, true>(items, n, n_sources, acc, counts, dig, status, s);
         return launch_lthash_chains<Items, false>(items, n, n_sources, acc, counts, dig, status, s);
+    }
+    // Samples of unknown or ragged length take the persistent lanes (a lane fetches its next sample the moment it
+    // finishes one: 2 M hellaswag-shaped samples 2.94 -> 1.09 ms unsorted, 40 k 93 -> 65 us); samples the caller
+    // declares to be of ONE length keep the plain grid, which has less bookkeeping per block (CIFAR 194 vs 217 us).
+    if constexpr (!Items::LONG_ITEMS) if (schedule == SNT_SCHEDULE_PERSISTENT && shape != SNT_SAMPLES_UNIFORM) {
+        if (smem_acc) return launch_lthash_lanes<Items, true>(items, n, n_sources, acc, counts, dig, status, s);
+        return launch_lthash_lanes<Items, false>(items, n, n_sources, acc, counts, dig, status, s);
     }
     const uint64_t grid = (n + LT_THREADS - 1) / LT_THREADS;
     if (grid > 0x7fffffffull) return SNT_ERR_INVALID_INPUT;
@@ -626,6 +659,15 @@ int snt_lthash_samples(const void* d_shard, const uint64_t* d_off, const uint64_
                        const uint64_t* d_ids, const uint32_t* d_slot, uint64_t n, uint32_t n_sources,
                        uint64_t* d_acc, uint64_t* d_counts, void* d_digests, uint64_t* d_status,
                        snt_stream_t stream) {
+    return snt_lthash_samples_shaped(d_shard, d_off, d_len, d_ids, d_slot, n, n_sources, d_acc, d_counts, d_digests,
+                                     d_status, SNT_SAMPLES_UNKNOWN, stream);
+}
+
+int snt_lthash_samples_shaped(const void* d_shard, const uint64_t* d_off, const uint64_t* d_len,
+                              const uint64_t* d_ids, const uint32_t* d_slot, uint64_t n, uint32_t n_sources,
+                              uint64_t* d_acc, uint64_t* d_counts, void* d_digests, uint64_t* d_status,
+                              uint32_t shape, snt_stream_t stream) {
+    if (shape > SNT_SAMPLES_RAGGED) return SNT_ERR_INVALID_INPUT;
     if (n_sources == 0 || !d_acc || !d_counts) return SNT_ERR_INVALID_INPUT;
     if (n && (!d_off || !d_len || !d_ids || !d_slot)) return SNT_ERR_INVALID_INPUT;
     SampleItems items;
@@ -635,7 +677,7 @@ int snt_lthash_samples(const void* d_shard, const uint64_t* d_off, const uint64_
     items.ids = d_ids;
     items.slot = d_slot;
     return launch_lthash(items, n, n_sources, d_acc, d_counts, d_digests, d_status,
-                         static_cast<cudaStream_t>(stream));
+                         static_cast<cudaStream_t>(stream), shape);
 }
 
 int snt_lthash_model(const snt_model_plan* plan, uint64_t leaf_begin, uint64_t leaf_end, uint64_t* d_acc,

@@ -32,11 +32,10 @@ from .errors import FormatError, ValidationError
 from .lattice import LatticeDigest, lt_add, lt_hash_block, lt_hash_tagged, lt_zero
 
 
-# Ragged datasets at least this large are hashed in length-sorted order. Measured on B200 with 2 M
-# hellaswag-shaped samples (tools/lthash_big_probe.py): the LtHash launch 2.93 -> 1.26 ms, the device argsort +
-# four row gathers 0.42 ms warm (the first argsort of a process also pays torch's one-time ~0.3 s sort set-up),
-# i.e. the sort pays for itself from roughly half a million samples; below a million it is not worth a branch.
-BALANCE_MIN_SAMPLES = 1 << 20
+def _all_equal(lengths: np.ndarray) -> bool:
+    """Do all samples have one length? Selects the launch (uniform samples: one thread per sample on a plain
+    grid; ragged ones: the persistent-lane kernel, which needs no length sort), never the result."""
+    return lengths.size == 0 or bool((lengths == lengths.flat[0]).all())
 
 
 def _checked_ids(ids) -> np.ndarray:
@@ -140,7 +139,8 @@ class _BatchEngine:
         done.record()
         self.stage_done[turn] = done
         self.acc.add_samples(d[header:], d[0:8 * n].view(torch.int64), d[8 * n:16 * n].view(torch.int64),
-                             d[16 * n:24 * n].view(torch.int64), d[24 * n:28 * n].view(torch.int32))
+                             d[16 * n:24 * n].view(torch.int64), d[24 * n:28 * n].view(torch.int32),
+                             uniform=_all_equal(lengths))
         self.pending = True
 
     def drain(self) -> Dict[int, Tuple[bytes, int]]:
@@ -226,9 +226,10 @@ class DeviceDataset:
     """
 
     def __init__(self, shard: torch.Tensor, offsets: torch.Tensor, lengths: torch.Tensor,
-                 ids: torch.Tensor, slots: torch.Tensor, source_ids: Sequence[int]):
+                 ids: torch.Tensor, slots: torch.Tensor, source_ids: Sequence[int], uniform: Optional[bool] = None):
         self.shard, self.offsets, self.lengths, self.ids, self.slots = shard, offsets, lengths, ids, slots
         self.source_ids = list(source_ids)
+        self.uniform = uniform           # all lengths equal? (None = not known; see LatticeAccumulator.add_samples)
 
     @property
     def n_samples(self) -> int:
@@ -263,27 +264,29 @@ class DeviceDataset:
         packed = torch.empty(max(n, 1) * 28, dtype=torch.uint8, pin_memory=True)
         view = packed.numpy()
         view[0:8 * n].view(np.uint64)[:] = np.asarray(offsets, dtype=np.uint64)
-        view[8 * n:16 * n].view(np.uint64)[:] = np.asarray(lengths, dtype=np.uint64)
+        lengths = np.asarray(lengths, dtype=np.uint64)
+        view[8 * n:16 * n].view(np.uint64)[:] = lengths
         view[16 * n:24 * n].view(np.uint64)[:] = np.asarray(ids, dtype=np.uint64)
         view[24 * n:28 * n].view(np.int32)[:] = slots.astype(np.int32, copy=False)
         rows = packed.to(dev, non_blocking=True)
         ds = cls(shard_t, rows[0:8 * n].view(torch.int64), rows[8 * n:16 * n].view(torch.int64),
-                 rows[16 * n:24 * n].view(torch.int64), rows[24 * n:28 * n].view(torch.int32), source_ids)
+                 rows[16 * n:24 * n].view(torch.int64), rows[24 * n:28 * n].view(torch.int32), source_ids,
+                 uniform=_all_equal(lengths))
         ds._staging = packed      # the pinned staging block outlives the asynchronous copy
         return ds
 
     def sorted_by_length(self) -> "DeviceDataset":
         """The same samples with the rows ordered by length (device-side argsort, shard untouched).
 
-        One thread hashes one sample, so a warp runs as long as its longest sample: with ragged
-        samples in arrival order half of the lanes idle. Per-source sums do not depend on the order
-        (dataset.py:67-71), so sorting the rows is free of semantics and makes every warp's lanes run
-        the same number of BLAKE2b compressions (2 M hellaswag-shaped samples: 2.93 -> 1.26 ms for 0.42 ms of
-        sorting, tools/lthash_big_probe.py). Worth it only for large ragged datasets (BALANCE_MIN_SAMPLES).
+        Per-source sums do not depend on the order (dataset.py:67-71). Round 1 hashed large ragged datasets
+        in this order because the one-thread-per-sample grid runs a warp as long as its longest sample
+        (2 M hellaswag-shaped samples: 2.94 ms unsorted, 1.26 ms sorted + 0.42 ms of sorting). The
+        persistent-lane kernel takes them unsorted in 1.09 ms (tools/lthash_lanes_probe.py), so nothing in the
+        package sorts any more; the method stays for callers that want length order for their own reasons.
         """
         order = torch.argsort(self.lengths)
         return DeviceDataset(self.shard, self.offsets[order], self.lengths[order], self.ids[order], self.slots[order],
-                             self.source_ids)
+                             self.source_ids, uniform=self.uniform)
 
     def accumulate(self, acc: "_dev.LatticeAccumulator", begin: int = 0, end: Optional[int] = None,
                    digests: Optional[torch.Tensor] = None) -> None:
@@ -292,7 +295,7 @@ class DeviceDataset:
         if end <= begin:
             return
         acc.add_samples(self.shard, self.offsets[begin:end], self.lengths[begin:end], self.ids[begin:end],
-                        self.slots[begin:end], digests)
+                        self.slots[begin:end], digests, uniform=self.uniform)
 
 
 def _finalize_device(acc: "_dev.LatticeAccumulator", source_ids: Sequence[int]) -> Dict[int, Tuple[LatticeDigest, int]]:
@@ -418,8 +421,6 @@ def digest_dataset(manifest: DatasetManifest, batch_size: int = 128, shuffle_see
         np.cumsum(ln[:-1], out=off[1:])
         shard = b"".join(parts)
     ds = DeviceDataset.from_host(shard, off.astype(np.uint64), ln.astype(np.uint64), ids, src, source_ids)
-    if n >= BALANCE_MIN_SAMPLES and int(ln.min()) != int(ln.max()):
-        ds = ds.sorted_by_length()
     acc = _dev.LatticeAccumulator(len(source_ids))
     ds.accumulate(acc)
     return _finalize_device(acc, ds.source_ids)
@@ -470,7 +471,7 @@ class StreamingDatasetHasher:
         slots = torch.where(self._table[pos] == src, pos, torch.full_like(pos, len(self.source_ids))).to(torch.int32)
         if flat.numel() == 0:
             flat = torch.zeros(16, dtype=torch.uint8, device=self._dev)
-        self._acc.add_samples(flat, off, ln, ids, slots)
+        self._acc.add_samples(flat, off, ln, ids, slots, uniform=True)      # rows of one tensor: one length
 
     def finalize(self) -> Dict[int, Tuple[LatticeDigest, int]]:
         """Per-source digests and counts, ordered by source id; raises if any batch named an undeclared source."""

@@ -560,13 +560,17 @@ class LatticeAccumulator:
         self.state.zero_()
 
     def add_samples(self, shard: torch.Tensor, offsets: torch.Tensor, lengths: torch.Tensor,
-                    ids: torch.Tensor, slots: torch.Tensor, digests: Optional[torch.Tensor] = None) -> None:
+                    ids: torch.Tensor, slots: torch.Tensor, digests: Optional[torch.Tensor] = None,
+                    uniform: Optional[bool] = None) -> None:
+        """``uniform``: what the caller knows about ``lengths`` (True = all equal, False = ragged, None =
+        unknown); it only selects the launch (``snt_lthash_samples_shaped``), never the result."""
         lib = _native.load()
         n = int(offsets.numel())
-        rc = lib.snt_lthash_samples(_ptr(shard), _ptr(offsets), _ptr(lengths), _ptr(ids), _ptr(slots), n,
-                                    self.n_sources, _ptr(self.acc), _ptr(self.counts), _ptr(digests),
-                                    _ptr(self.status), _stream())
-        _native.check(rc, "snt_lthash_samples")
+        shape = _native.SAMPLES_UNKNOWN if uniform is None else (_native.SAMPLES_UNIFORM if uniform else _native.SAMPLES_RAGGED)
+        rc = lib.snt_lthash_samples_shaped(_ptr(shard), _ptr(offsets), _ptr(lengths), _ptr(ids), _ptr(slots), n,
+                                           self.n_sources, _ptr(self.acc), _ptr(self.counts), _ptr(digests),
+                                           _ptr(self.status), shape, _stream())
+        _native.check(rc, "snt_lthash_samples_shaped")
 
     def add_model_leaves(self, plan: ModelPlan, leaf_begin: int, leaf_end: int,
                          digests: Optional[torch.Tensor] = None) -> None:

@@ -89,7 +89,7 @@ def _hash_one(tag: bytes, data) -> LatticeDigest:
         ids = torch.from_numpy(np.frombuffer(tag, dtype=np.int64).copy()).to(dev)
         slot = torch.zeros(1, dtype=torch.int32, device=dev)
         out = torch.empty(64, dtype=torch.uint8, device=dev)
-        acc.add_samples(shard, off, ln, ids, slot, digests=out)
+        acc.add_samples(shard, off, ln, ids, slot, digests=out, uniform=True)
         return LatticeDigest(out.cpu().numpy().tobytes())
     from .compression import CompressionAlg
     from .merkle import hash_blocks

@@ -44,7 +44,7 @@ def test_header_cites_the_reference_interface():
 
 
 def test_constants_and_strings(lib):
-    assert lib.snt_abi_version() == 2
+    assert lib.snt_abi_version() == 3
     assert [lib.snt_digest_len(a) for a in (0, 1, 2, 3)] == [32, 64, 32, 0]
     assert lib.snt_strerror(0) == b"ok"
     assert b"invalid input" in lib.snt_strerror(-1)

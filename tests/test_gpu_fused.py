@@ -212,6 +212,49 @@ def test_lthash_chain_kernel_matches_grid_and_oracle(dev, corc):
             assert dig == want_dig, (n, schedule)
 
 
+def test_lthash_lanes_kernel_block_boundaries_and_alignments(dev, corc):
+    """The persistent-lane LtHash kernel (default for samples of unknown / ragged length) against the C oracle on the
+    lengths where its staging changes shape -- around every 128-byte chunk edge with the 8-byte tag in front (a
+    sample of 120 bytes fills block 0 exactly, 121 needs a second block whose data chunk is empty) -- at 8-byte,
+    4-byte and odd addresses (cp.async 8 / cp.async 4 / register path), with fewer samples than lanes, exactly one
+    ring refill, and many samples per lane; the length hint must never change a result."""
+    from paper_2510_00554_b200 import _native
+
+    lib = _native.load()
+    assert lib.snt_merkle_schedule(_native.SCHEDULE_PERSISTENT) == 0
+    rng = np.random.default_rng(77)
+    edge = np.array([0, 1, 7, 8, 9, 119, 120, 121, 127, 128, 129, 247, 248, 249, 255, 256, 257, 1016, 1024, 3072, 5000],
+                    dtype=np.uint64)
+    for n, align in ((len(edge), 8), (len(edge), 4), (len(edge), 1), (64, 4), (96, 8), (3000, 4), (20000, 1)):
+        lens = edge.copy() if n == len(edge) else rng.choice(edge[:17], size=n).astype(np.uint64)
+        offs = np.zeros(n, dtype=np.uint64)
+        pos = 0
+        for i in range(n):
+            pos = -(-pos // align) * align
+            if align == 1 and i % 2:
+                pos += 1 + (i % 3)                               # odd addresses
+            if align == 4 and i % 2 and pos % 8 == 0:
+                pos += 4                                         # 4-byte aligned but not 8
+            offs[i] = pos
+            pos += int(lens[i])
+        shard = rng.integers(0, 256, size=pos + 16, dtype=np.uint8)
+        n_src = 5
+        slots = rng.integers(0, n_src, size=n).astype(np.uint32)
+        ids = rng.integers(0, 2**63, size=n).astype(np.uint64)
+        want_sums, want_counts, want_dig = corc.lthash_samples(shard, offs, lens, ids, slots, n_src, 4, want_digests=True)
+        d_shard = torch.from_numpy(shard).cuda()
+        d_off, d_len, d_ids = (torch.from_numpy(a.view(np.int64)).cuda() for a in (offs, lens, ids))
+        d_slots = torch.from_numpy(slots.view(np.int32)).cuda()
+        for uniform in (None, False, True):                      # unknown and ragged: lanes; "uniform" (a lie here): the grid
+            acc = dev.LatticeAccumulator(n_src)
+            dig = torch.zeros(n * 64, dtype=torch.uint8, device="cuda")
+            acc.add_samples(d_shard, d_off, d_len, d_ids, d_slots, dig, uniform=uniform)
+            out, counts, status = acc.digests()
+            assert (status, counts) == (0, list(want_counts)), (n, align, uniform)
+            assert out == want_sums, (n, align, uniform)
+            assert dig.cpu().numpy().tobytes() == want_dig, (n, align, uniform)
+
+
 def test_resident_model_cache_revalidates_every_call(porc):
     """hash_model on a TensorMap of CUDA tensors re-uses plan and workspace, launches before it re-checks the tensors,
     and still never returns a digest for bytes it did not check: content changes, re-pointed tensors, resized tensors

@@ -4,9 +4,10 @@
 
 All three Merkle schedules (persistent chains + reducer, fused single launch, grid) on ragged / unaligned models
 whose SMs get more chains than worker warps (so the parked-state FIFO runs), shard ranges with forced levels, and
-the LtHash kernels (grid and forced chains). Results are checked against hashlib, so a silent corruption fails too.
+the LtHash kernels (grid, forced chains, persistent lanes). SANITIZE_ONLY=lthash skips the Merkle part. Results are checked against hashlib, so a silent corruption fails too.
 """
 import hashlib
+import os
 import sys
 from pathlib import Path
 
@@ -43,7 +44,7 @@ host = [arena_h[a:b].tobytes() for a, b in zip(cuts[:-1], cuts[1:])]
 blocks = [t[o:o + bs] for t in host for o in range(0, len(t), bs)]
 plan = dev.ModelPlan(views, bs)
 assert plan.leaf_count == len(blocks)
-for alg in ("sha256", "blake2b", "sha3-256"):
+for alg in (() if os.environ.get("SANITIZE_ONLY") == "lthash" else ("sha256", "blake2b", "sha3-256")):
     want_leaves = [H[alg](b).digest() for b in blocks]
     want_root = merkle_root(alg, want_leaves)
     for schedule in (_native.SCHEDULE_PERSISTENT, _native.SCHEDULE_FUSED, _native.SCHEDULE_GRID):
@@ -79,7 +80,7 @@ for i in range(n):
 want = (want & 0xFFFF).astype("<u2").tobytes()
 d_args = [torch.from_numpy(shard_h).cuda()] + [torch.from_numpy(a.view(np.int64)).cuda() for a in (offs, lens, ids)] + \
          [torch.from_numpy(slots).cuda()]
-for schedule in (_native.SCHEDULE_FUSED, _native.SCHEDULE_GRID):
+for schedule in (_native.SCHEDULE_FUSED, _native.SCHEDULE_GRID, _native.SCHEDULE_PERSISTENT):   # chains, grid, lanes
     lib.snt_merkle_schedule(schedule)
     acc = dev.LatticeAccumulator(n_src)
     acc.add_samples(*d_args)
