@@ -97,7 +97,10 @@ int sm_count() {
 // Worker warps per persistent CTA, upper bound per algorithm (registers: 65,536 / (32 * W)).
 constexpr int FUSED_MAXW_SHA256 = SNT_FUSED_MAXW_SHA256;
 constexpr int FUSED_MAXW_WIDE = 16;      // SHA3-256
-constexpr int FUSED_MAXW_BLAKE2B = 8;    // fewer, fatter warps: 34 KB of unrolled rounds per warp position, 128+ registers
+#ifndef SNT_FUSED_MAXW_BLAKE2B
+#define SNT_FUSED_MAXW_BLAKE2B 8
+#endif
+constexpr int FUSED_MAXW_BLAKE2B = SNT_FUSED_MAXW_BLAKE2B;    // fewer, fatter warps: 34 KB of unrolled rounds per warp position, 128+ registers
 size_t align256(size_t x) { return (x + 255) & ~static_cast<size_t>(255); }
 
 // Workspace of one (algorithm, node count): [ping-pong levels of the multi-launch reducer | completion

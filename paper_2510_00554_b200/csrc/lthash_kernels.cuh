@@ -18,6 +18,10 @@
 
 namespace snt {
 
+#ifndef SNT_LT_GRID_ROLLED
+#define SNT_LT_GRID_ROLLED 0
+#endif
+constexpr bool LT_GRID_ROLLED = SNT_LT_GRID_ROLLED != 0;   // grid kernel compresses from the staging buffer (compress_staged)
 constexpr int LT_THREADS = 64;
 constexpr int LT_LANES = 32;                 // u16 lanes per digest
 constexpr int LT_SMEM_SOURCES = 128;         // per-CTA shared accumulators: 128 x 32 x 4 B = 16 KiB
@@ -114,7 +118,7 @@ lthash_kernel(const Items items, uint64_t n, uint32_t n_sources, unsigned long l
             if (status) atomicAdd(status, 1ull);       // undeclared source (dataset.py:78-80): counted, skipped
         } else {
             uint64_t h[8];
-            Blake2bStaged<LT_THREADS>::template hash_message<Items::TAG_WORDS>(stage, it.tag, it.tag1, it.ptr, it.len, h);
+            Blake2bStaged<LT_THREADS>::template hash_message<Items::TAG_WORDS, LT_GRID_ROLLED>(stage, it.tag, it.tag1, it.ptr, it.len, h);
             if (digests) {
                 uint4* o = reinterpret_cast<uint4*>(digests + i * 64);
 #pragma unroll

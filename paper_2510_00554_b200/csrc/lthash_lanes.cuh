@@ -32,58 +32,6 @@ constexpr size_t LTL_QUEUE_BYTES = LTL_QCAP * 64ull + LTL_QCAP * sizeof(uint32_t
 SNT_HD constexpr size_t ltl_ring_bytes(int tag_words) { return (2ull + tag_words) * LTL_RING * sizeof(uint64_t) + LTL_RING * sizeof(uint32_t); }
 SNT_HD constexpr size_t ltl_warp_bytes(int tag_words) { return LTL_STAGE_BYTES_PER_WARP + ltl_ring_bytes(tag_words) + LTL_QUEUE_BYTES; }
 
-// Byte offset of message word sigma[r][j] inside a lane-strided staging buffer (slots 256 bytes apart).
-#define LTL_O(x) (x) * 256
-#define LTL_ROW(a, b, c, d, e, f, g, h, i, j, k, l, m, n, o, p) \
-    {LTL_O(a), LTL_O(b), LTL_O(c), LTL_O(d), LTL_O(e), LTL_O(f), LTL_O(g), LTL_O(h), \
-     LTL_O(i), LTL_O(j), LTL_O(k), LTL_O(l), LTL_O(m), LTL_O(n), LTL_O(o), LTL_O(p)}
-__constant__ uint32_t c_ltl_sigma_off[12][16] = {
-    LTL_ROW(0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15),
-    LTL_ROW(14, 10, 4, 8, 9, 15, 13, 6, 1, 12, 0, 2, 11, 7, 5, 3),
-    LTL_ROW(11, 8, 12, 0, 5, 2, 15, 13, 10, 14, 3, 6, 7, 1, 9, 4),
-    LTL_ROW(7, 9, 3, 1, 13, 12, 11, 14, 2, 6, 5, 10, 4, 0, 15, 8),
-    LTL_ROW(9, 0, 5, 7, 2, 4, 10, 15, 14, 1, 11, 12, 6, 8, 3, 13),
-    LTL_ROW(2, 12, 6, 10, 0, 11, 8, 3, 4, 13, 7, 5, 15, 14, 1, 9),
-    LTL_ROW(12, 5, 1, 15, 14, 13, 4, 10, 0, 7, 6, 3, 9, 2, 8, 11),
-    LTL_ROW(13, 11, 7, 14, 12, 1, 3, 9, 5, 0, 15, 4, 8, 6, 2, 10),
-    LTL_ROW(6, 15, 14, 9, 11, 3, 0, 8, 12, 2, 13, 7, 1, 4, 10, 5),
-    LTL_ROW(10, 2, 8, 4, 7, 6, 1, 5, 15, 11, 9, 14, 3, 12, 13, 0),
-    LTL_ROW(0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15),
-    LTL_ROW(14, 10, 4, 8, 9, 15, 13, 6, 1, 12, 0, 2, 11, 7, 5, 3)};
-#undef LTL_ROW
-#undef LTL_O
-
-// One BLAKE2b compression with the message block left in shared memory (lane-strided staging buffer `cur`):
-// the twelve rounds are ONE loop body that fetches its sixteen message words in sigma order with LDS at
-// offsets from the constant bank. 3 KB of code instead of the 34 KB of the unrolled rounds -- with twelve warps
-// per SM at twelve different places of a 55 KB kernel the instruction cache was the top stall (ncu:
-// no_instruction 22 % of the samples) -- and no 32 registers of message.
-struct Blake2bLanes : Blake2b {
-SNT_D static void compress_staged(uint64_t h[8], const uint64_t* cur, uint64_t t, bool last) {
-    uint64_t v0 = h[0], v1 = h[1], v2 = h[2], v3 = h[3], v4 = h[4], v5 = h[5], v6 = h[6], v7 = h[7];
-    uint64_t v8 = SNT_B2B_IV0, v9 = SNT_B2B_IV1, v10 = SNT_B2B_IV2, v11 = SNT_B2B_IV3;
-    uint64_t v12 = SNT_B2B_IV4 ^ t, v13 = SNT_B2B_IV5;
-    uint64_t v14 = last ? ~SNT_B2B_IV6 : SNT_B2B_IV6, v15 = SNT_B2B_IV7;
-    const char* base = reinterpret_cast<const char*>(cur);
-#pragma unroll 1
-    for (int r = 0; r < 12; ++r) {
-        uint64_t m[16];
-#pragma unroll
-        for (int j = 0; j < 16; ++j) m[j] = *reinterpret_cast<const uint64_t*>(base + c_ltl_sigma_off[r][j]);
-        SNT_B2B_G(v0, v4, v8, v12, m[0], m[1]);
-        SNT_B2B_G(v1, v5, v9, v13, m[2], m[3]);
-        SNT_B2B_G(v2, v6, v10, v14, m[4], m[5]);
-        SNT_B2B_G(v3, v7, v11, v15, m[6], m[7]);
-        SNT_B2B_G(v0, v5, v10, v15, m[8], m[9]);
-        SNT_B2B_G(v1, v6, v11, v12, m[10], m[11]);
-        SNT_B2B_G(v2, v7, v8, v13, m[12], m[13]);
-        SNT_B2B_G(v3, v4, v9, v14, m[14], m[15]);
-    }
-    h[0] ^= v0 ^ v8;  h[1] ^= v1 ^ v9;  h[2] ^= v2 ^ v10; h[3] ^= v3 ^ v11;
-    h[4] ^= v4 ^ v12; h[5] ^= v5 ^ v13; h[6] ^= v6 ^ v14; h[7] ^= v7 ^ v15;
-}
-};
-
 SNT_D void ltl_cp8(uint64_t* dst, const uint8_t* src) {
     const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
@@ -288,7 +236,7 @@ lthash_lanes_kernel(const Items items, uint64_t n, uint32_t n_sources, unsigned 
                 for (int i = 0; i < T; ++i) other[i * 32] = cur[(16 + i) * 32];   // words carried into the next block
             }
             tcnt += 128;
-            Blake2bLanes::compress_staged(h, cur, last ? total : tcnt, last);
+            Blake2bStaged<32>::compress_staged(h, cur, last ? total : tcnt, last);
             sp += 128;
             srem = srem > 128 ? srem - 128 : 0;
             --left;

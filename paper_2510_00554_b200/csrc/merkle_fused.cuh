@@ -33,6 +33,9 @@
 // packed 32 to a chain of their own, hashed through the out-of-line generic path at the front of an
 // SM's queue, and signal their groups leaf by leaf.
 #pragma once
+#ifndef SNT_MERKLE_B2B_ROLLED
+#define SNT_MERKLE_B2B_ROLLED 0      // BLAKE2b leaf loop: unrolled rounds from registers (1) = rolled rounds from the staging buffer
+#endif
 #include "chain_sched.cuh"
 #include "merkle_kernels.cuh"
 
@@ -404,7 +407,7 @@ merkle_fused_kernel(const __grid_constant__ FusedArgs a, const __grid_constant__
 #pragma unroll
                     for (int i = 0; i < 8; ++i) h[i] = (static_cast<uint64_t>(s[2 * i + 1]) << 32) | s[2 * i];
                     uint64_t* stage = reinterpret_cast<uint64_t*>(fused_smem) + threadIdx.x;
-                    Blake2bStaged<MAXW * 32>::template hash_blocks<0>(stage, 0, 0, leaf.ptr, leaf.len, u0, u1, h);
+                    Blake2bStaged<MAXW * 32>::template hash_blocks<0, SNT_MERKLE_B2B_ROLLED != 0>(stage, 0, 0, leaf.ptr, leaf.len, u0, u1, h);
 #pragma unroll
                     for (int i = 0; i < 8; ++i) { s[2 * i] = static_cast<uint32_t>(h[i]); s[2 * i + 1] = static_cast<uint32_t>(h[i] >> 32); }
                 } else {
