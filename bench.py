@@ -376,6 +376,54 @@ def gpu_model_config(pkg, dev, shapes, arch, alg, device, steps, hbm_peak, peak_
     return out
 
 
+def lattice_model_config(pkg, dev, shapes, arch, device, steps, hbm_peak, peak_src, peaks, ref, cores):
+    """LATTICE in-place model hashing (reference model.py:312-315): every 8 KiB block hashed as
+    BLAKE2b-512(LE64(k) || block), the u16 lanes summed into ONE 64-byte digest. GPU time and roofline; with `ref`
+    the reference package on the same bytes (digest asserted)."""
+    import torch
+
+    sd = shapes.synthetic_state_dict(arch, device, seed=0)
+    plan = dev.ModelPlan([dev.as_device_bytes(t) for _, t in sd], BLOCK)
+    acc = dev.LatticeAccumulator(1)
+
+    def step():
+        acc.zero_()
+        acc.add_model_leaves(plan, 0, plan.leaf_count)
+
+    step_ms = cuda_time_ms(step, steps, 3)
+    step()
+    digest, counts, _ = acc.digests()
+    assert counts == [plan.leaf_count]
+    cfg = pkg.HashConfig(pkg.Construction.LATTICE, pkg.Strategy.IN_PLACE, pkg.CompressionAlg.BLAKE2B)
+    api = pkg.hash_model(cfg, pkg.TensorMap([(name, t) for name, t in sd]))
+    assert api.model_digest.data == digest
+    achieved = plan.total_bytes / (step_ms * 1e-3) / 1e9
+    blocks = plan.leaf_count * 65                      # 8 + 8192 bytes = 65 BLAKE2b blocks per full leaf (upper bound for ragged tails)
+    roof = {"bound": "hbm", "kernel": "lthash kernel over model blocks (BLAKE2b per block + lane sums)", "achieved": round(achieved, 1),
+            "peak": hbm_peak, "unit": "GB/s", "frac": round(achieved / hbm_peak, 4), "traffic": None, "peak_source": peak_src,
+            "kernel_ms": round(step_ms, 4), "algorithmic_bytes": plan.total_bytes}
+    if peaks and "error" not in peaks:
+        alu_peak = max(peaks["lop3_tops"], peaks["shf_tops"], peaks["iadd3_tops"])
+        roof.update({"binding_unit": "integer ALU pipe",
+                     "binding_unit_frac": round(LT_ALU_PER_BLOCK * blocks / (step_ms * 1e-3) / 1e12 / alu_peak, 4)})
+    out = {"workload": f"{arch} (random-init fp32) LATTICE in-place model hash (LtHash over 8 KiB blocks), block {BLOCK}",
+           "arch": arch, "alg": "lthash-blake2b", "bytes": plan.total_bytes, "leaves": plan.leaf_count, "tensors": len(sd),
+           "ms_per_step": round(step_ms, 4), "value": round(plan.total_bytes / step_ms / 1e6, 2), "unit": UNIT,
+           "digest": digest.hex()[:32], "roofline": roof}
+    if ref is not None:
+        host = host_views(sd)
+        rcfg = ref.HashConfig(ref.Construction.LATTICE, ref.Strategy.IN_PLACE, ref.CompressionAlg.BLAKE2B, BLOCK)
+        dt, res = timed_cpu(lambda: ref.hash_model(rcfg, reference_model(ref, host), workers=cores))
+        assert res.model_digest.data == digest, f"{arch}: GPU lattice digest differs from the reference package's"
+        out["cpu_baseline"] = {"value": round(plan.total_bytes / dt / 1e9, 4), "unit": UNIT, "cores": cores, "kind": "reference",
+                               "ms": round(dt * 1e3, 1), "parity": "64-byte lattice digest identical",
+                               "sample": f"sentinel.hash_model(LATTICE, IN_PLACE, workers={cores}) over the D2H copy of the full state dict, one pass"}
+    plan.close()
+    del plan, sd, acc
+    torch.cuda.empty_cache()
+    return out
+
+
 def cifar_shaped(np):
     n, ln, n_src = 50_000, 3072, 16
     data = np.random.default_rng(0).integers(0, 256, size=n * ln, dtype=np.uint8)
@@ -769,10 +817,13 @@ def run_ours(args):
             plan.close()
             del plan, flat, sd
             torch.cuda.empty_cache()
-            for arch, alg in (("gpt2", "sha256"), ("bert-large", "blake2b"), ("bert-large", "sha3-256"),
+            for arch, alg in (("gpt2", "sha256"), ("gpt2-model", "sha256"), ("bert-large", "blake2b"), ("bert-large", "sha3-256"),
                               ("vgg19", "blake2b"), ("vgg19", "sha3-256")):
                 configs.append(gpu_model_config(pkg, dev, shapes, arch, alg, device, args.steps, hbm_peak, peak_src, peaks,
                                                 ref, cores, traffic_db))
+            configs.append(lattice_model_config(pkg, dev, shapes, "gpt2", device, args.steps, hbm_peak, peak_src, peaks, ref, cores))
+            # GPT2-XL: GPU time only (the reference's LATTICE pass over 6.55 GB takes ~20 s; parity at full size is in tests/)
+            configs.append(lattice_model_config(pkg, dev, shapes, "gpt2-xl", device, args.steps, hbm_peak, peak_src, peaks, None, cores))
         cifar, _ = dataset_config("cifar10_shaped", "CIFAR10-shaped synthetic dataset (50,000 x 3,072 B uint8, 16 sources) LtHash",
                                   cifar_shaped(np), np, torch, dsm, dev, dd, world, rank, args.steps, args.warmup, barrier,
                                   device, hbm_peak, peak_src, peaks, ref, cores)

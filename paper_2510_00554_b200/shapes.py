@@ -36,6 +36,13 @@ def gpt2_lm_head(n_embd: int = 768, n_layer: int = 12, vocab: int = 50257, n_pos
     return out
 
 
+def gpt2_model(n_embd: int = 768, n_layer: int = 12, vocab: int = 50257, n_pos: int = 1024) -> Layout:
+    """``GPT2Model`` (no LM head): the LM-head layout without ``lm_head.weight`` and without the ``transformer.``
+    prefix -- 148 / 580 entries, the "124M" / "1.5B" parameter counts."""
+    return [(name[len("transformer."):], shape, alias) for name, shape, alias in gpt2_lm_head(n_embd, n_layer, vocab, n_pos)
+            if name != "lm_head.weight"]
+
+
 def bert_model(hidden: int = 1024, layers: int = 24, intermediate: int = 4096, vocab: int = 30522,
                max_pos: int = 512, type_vocab: int = 2) -> Layout:
     h = hidden
@@ -109,6 +116,8 @@ def resnet_bottleneck(blocks=(3, 8, 36, 3), num_classes: int = 1000) -> Layout:
 ARCHITECTURES = {
     "gpt2": lambda: gpt2_lm_head(768, 12),
     "gpt2-xl": lambda: gpt2_lm_head(1600, 48),
+    "gpt2-model": lambda: gpt2_model(768, 12),
+    "gpt2-xl-model": lambda: gpt2_model(1600, 48),
     "bert-large": lambda: bert_model(1024, 24, 4096),
     "vgg19": vgg19,
     "bert-base": lambda: bert_model(768, 12, 3072),

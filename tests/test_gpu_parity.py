@@ -326,6 +326,25 @@ def test_full_size_models_against_c_oracle(pkg, corc, arch, alg):
     assert res.model_digest.data == hasher.out_bytes()
 
 
+@pytest.mark.parametrize("arch", ["gpt2", "bert-large"])
+def test_full_size_lattice_model_against_c_oracle(pkg, corc, arch):
+    """LATTICE in-place hashing at full model size, through both LtHash schedules for model blocks
+    (persistent chains, plain grid), against the multi-threaded C oracle."""
+    from paper_2510_00554_b200 import _native
+
+    sd = _synthetic(arch)
+    host = [t.reshape(-1).view(torch.uint8).cpu().numpy() for _, t in sd]
+    want = corc.inplace_lattice(corc.TensorList(host), 8192, corc.threads_default())
+    cfg = pkg.HashConfig(pkg.Construction.LATTICE, pkg.Strategy.IN_PLACE, pkg.CompressionAlg.BLAKE2B, 8192)
+    lib = _native.load()
+    try:
+        for schedule in (_native.SCHEDULE_PERSISTENT, _native.SCHEDULE_GRID):
+            lib.snt_merkle_schedule(schedule)
+            assert pkg.hash_model(cfg, pkg.TensorMap(list(sd))).model_digest.data == want, schedule
+    finally:
+        lib.snt_merkle_schedule(_native.SCHEDULE_PERSISTENT)
+
+
 def test_shard_roots_recombine_to_whole_root(pkg):
     """Size-independent property of the multi-GPU rule, on one GPU at GPT-2-small size."""
     from paper_2510_00554_b200 import device as dev

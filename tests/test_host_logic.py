@@ -155,6 +155,8 @@ def test_dataset_manifest_round_trip_and_validation(tmp_path):
 @pytest.mark.parametrize("arch,entries,nbytes,leaves,ragged", [
     ("gpt2", 149, 652_148_736, 79_672, 100),
     ("gpt2-xl", 581, 6_552_089_600, 799_954, 388),
+    ("gpt2-model", 148, 497_759_232, 60_825, 99),
+    ("gpt2-xl-model", 580, 6_230_444_800, 760_690, 387),
     ("bert-large", 391, 1_340_567_552, 163_753, 219),
     ("vgg19", 38, 574_668_960, 70_164, 18),
     ("bert-base", 199, 437_928_960, 53_534, 125),          # SURVEY.md section 8, context rows
