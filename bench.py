@@ -398,14 +398,21 @@ def lattice_model_config(pkg, dev, shapes, arch, device, steps, hbm_peak, peak_s
     api = pkg.hash_model(cfg, pkg.TensorMap([(name, t) for name, t in sd]))
     assert api.model_digest.data == digest
     achieved = plan.total_bytes / (step_ms * 1e-3) / 1e9
-    blocks = plan.leaf_count * 65                      # 8 + 8192 bytes = 65 BLAKE2b blocks per full leaf (upper bound for ragged tails)
+    # BLAKE2b blocks: ceil((8 + leaf bytes) / 128) per leaf -- 65 for a full 8 KiB leaf, fewer for a tensor's ragged tail
+    blocks = 0
+    for _, t in sd:
+        nb = t.numel() * t.element_size()
+        full, tail = divmod(nb, BLOCK)
+        blocks += full * ((8 + BLOCK + 127) // 128) + (((8 + tail + 127) // 128) if tail else 0)
     roof = {"bound": "hbm", "kernel": "lthash kernel over model blocks (BLAKE2b per block + lane sums)", "achieved": round(achieved, 1),
             "peak": hbm_peak, "unit": "GB/s", "frac": round(achieved / hbm_peak, 4), "traffic": None, "peak_source": peak_src,
             "kernel_ms": round(step_ms, 4), "algorithmic_bytes": plan.total_bytes}
     if peaks and "error" not in peaks:
         alu_peak = max(peaks["lop3_tops"], peaks["shf_tops"], peaks["iadd3_tops"])
         roof.update({"binding_unit": "integer ALU pipe",
-                     "binding_unit_frac": round(LT_ALU_PER_BLOCK * blocks / (step_ms * 1e-3) / 1e12 / alu_peak, 4)})
+                     # per-block count of the unrolled BLAKE2b compression the chain kernel runs (SASS, as ALU_PER_LEAF)
+                     "binding_unit_frac": round(ALU_PER_LEAF["blake2b"] // 64 * blocks / (step_ms * 1e-3) / 1e12 / alu_peak, 4),
+                     "blake2b_blocks": blocks})
     out = {"workload": f"{arch} (random-init fp32) LATTICE in-place model hash (LtHash over 8 KiB blocks), block {BLOCK}",
            "arch": arch, "alg": "lthash-blake2b", "bytes": plan.total_bytes, "leaves": plan.leaf_count, "tensors": len(sd),
            "ms_per_step": round(step_ms, 4), "value": round(plan.total_bytes / step_ms / 1e6, 2), "unit": UNIT,
