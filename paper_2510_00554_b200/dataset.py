@@ -41,9 +41,9 @@ def _all_equal(lengths: np.ndarray) -> bool:
 def _checked_ids(ids) -> np.ndarray:
     """Sample ids as u64; an id outside [0, 2^64) is an error, as it is for the reference's
     ``struct.pack("<Q", sample_id)`` (dataset.py:45) -- never wrapped into another sample's tag."""
-    for i in ids:
-        if not 0 <= i < (1 << 64):
-            raise ValidationError(f"sample id {i} does not fit an unsigned 64-bit tag")
+    if ids and not (0 <= min(ids) and max(ids) < (1 << 64)):
+        i = next(i for i in ids if not 0 <= i < (1 << 64))
+        raise ValidationError(f"sample id {i} does not fit an unsigned 64-bit tag")
     return np.array(ids, dtype=np.uint64)
 
 
@@ -112,7 +112,7 @@ class _BatchEngine:
 
     def add(self, payloads: Sequence[bytes], ids: np.ndarray, source_ids: Sequence[int]) -> None:
         n = len(payloads)
-        lengths = np.fromiter((len(p) for p in payloads), dtype=np.uint64, count=n)
+        lengths = np.fromiter(map(len, payloads), dtype=np.uint64, count=n)
         total = int(lengths.sum())
         header = -(-28 * n // self.HEADER_ALIGN) * self.HEADER_ALIGN
         need = header + max(total, 16)
@@ -131,7 +131,11 @@ class _BatchEngine:
         np.cumsum(lengths[:-1], out=offsets[1:])
         view[8 * n:16 * n].view(np.uint64)[:] = lengths
         view[16 * n:24 * n].view(np.uint64)[:] = ids
-        view[24 * n:28 * n].view(np.int32)[:] = [self._slot(s) for s in source_ids]
+        try:
+            slots = list(map(self.slot_of.__getitem__, source_ids))      # sources seen before: one dict lookup each
+        except KeyError:
+            slots = [self._slot(s) for s in source_ids]
+        view[24 * n:28 * n].view(np.int32)[:] = slots
         view[header:header + total] = np.frombuffer(b"".join(payloads), dtype=np.uint8)
         d = self.d_block
         d[:need].copy_(self.stage[turn][:need], non_blocking=True)
@@ -312,16 +316,18 @@ def process_batch(batch: Batch, acc: SourceAccumulator) -> SourceAccumulator:
     one launch into sums that stay on the device; the call returns without waiting for the GPU. The
     host-side ``acc.sums`` / ``acc.counts`` catch up when they are read (``finalize`` does).
     """
-    for s in batch.samples:
-        if acc.declared_sources is not None and s.source_id not in acc.declared_sources:
-            raise ValidationError(f"sample {s.sample_id} references undeclared source {s.source_id}")
-    if not batch.samples:
+    samples = batch.samples
+    source_ids = [s.source_id for s in samples]
+    if acc.declared_sources is not None and not acc.declared_sources.issuperset(source_ids):
+        s = next(s for s in samples if s.source_id not in acc.declared_sources)
+        raise ValidationError(f"sample {s.sample_id} references undeclared source {s.source_id}")
+    if not samples:
         return acc
-    payloads = [(s.label + s.data) if acc.cover_labels else s.data for s in batch.samples]
-    ids = _checked_ids([s.sample_id for s in batch.samples])
+    payloads = [s.label + s.data for s in samples] if acc.cover_labels else [s.data for s in samples]
+    ids = _checked_ids([s.sample_id for s in samples])
     if acc._engine is None:
         acc._engine = _BatchEngine()
-    acc._engine.add(payloads, ids, [s.source_id for s in batch.samples])
+    acc._engine.add(payloads, ids, source_ids)
     return acc
 
 
