@@ -376,7 +376,7 @@ def gpu_model_config(pkg, dev, shapes, arch, alg, device, steps, hbm_peak, peak_
     return out
 
 
-def lattice_model_config(pkg, dev, shapes, arch, device, steps, hbm_peak, peak_src, peaks, ref, cores):
+def lattice_model_config(pkg, dev, shapes, arch, device, steps, hbm_peak, peak_src, peaks, ref, cores, traffic_db=None):
     """LATTICE in-place model hashing (reference model.py:312-315): every 8 KiB block hashed as
     BLAKE2b-512(LE64(k) || block), the u16 lanes summed into ONE 64-byte digest. GPU time and roofline; with `ref`
     the reference package on the same bytes (digest asserted)."""
@@ -405,7 +405,8 @@ def lattice_model_config(pkg, dev, shapes, arch, device, steps, hbm_peak, peak_s
         full, tail = divmod(nb, BLOCK)
         blocks += full * ((8 + BLOCK + 127) // 128) + (((8 + tail + 127) // 128) if tail else 0)
     roof = {"bound": "hbm", "kernel": "lthash kernel over model blocks (BLAKE2b per block + lane sums)", "achieved": round(achieved, 1),
-            "peak": hbm_peak, "unit": "GB/s", "frac": round(achieved / hbm_peak, 4), "traffic": None, "peak_source": peak_src,
+            "peak": hbm_peak, "unit": "GB/s", "frac": round(achieved / hbm_peak, 4),
+            "traffic": (traffic_db or {}).get(f"lthash_chain_kernel:{arch}"), "peak_source": peak_src,
             "kernel_ms": round(step_ms, 4), "algorithmic_bytes": plan.total_bytes}
     if peaks and "error" not in peaks:
         alu_peak = max(peaks["lop3_tops"], peaks["shf_tops"], peaks["iadd3_tops"])
@@ -468,7 +469,7 @@ def reference_dataset_digests(ref, shard, offs, lens, ids, src, n_src, batch=128
 
 
 def dataset_config(name, workload, arrays, np, torch, dsm, dev, dd, world, rank, steps, warmup, barrier, device,
-                   hbm_peak, peak_src, peaks, ref, cores):
+                   hbm_peak, peak_src, peaks, ref, cores, traffic_db=None):
     """A LtHash dataset configuration: device-resident samples/s, end to end from pinned host memory, the
     reference loop on the same samples (per-source digests and counts asserted), roofline of the kernel."""
     import torch.distributed as dist
@@ -530,7 +531,9 @@ def dataset_config(name, workload, arrays, np, torch, dsm, dev, dd, world, rank,
     kernel_name = ("lthash_kernel (one thread per sample: samples of one length)" if dset.uniform else
                    "lthash_lanes_kernel (persistent lanes: ragged samples, no sort)")
     roof = {"bound": "hbm", "kernel": kernel_name + ", BLAKE2b per sample + per-source lane sums", "achieved": round(achieved, 1),
-            "peak": hbm_peak, "unit": "GB/s", "frac": round(achieved / hbm_peak, 4), "traffic": None, "peak_source": peak_src,
+            "peak": hbm_peak, "unit": "GB/s", "frac": round(achieved / hbm_peak, 4),
+            "traffic": (traffic_db or {}).get(("lthash_kernel:" if dset.uniform else "lthash_lanes_kernel:") + name) if world == 1 else None,
+            "peak_source": peak_src,
             "kernel_ms": round(kernel_ms, 4), "share_of_step": round(kernel_ms / ds_ms, 4), "algorithmic_bytes": my_bytes}
     if peaks and "error" not in peaks:
         alu_peak = max(peaks["lop3_tops"], peaks["shf_tops"], peaks["iadd3_tops"])
@@ -828,17 +831,18 @@ def run_ours(args):
                               ("vgg19", "blake2b"), ("vgg19", "sha3-256")):
                 configs.append(gpu_model_config(pkg, dev, shapes, arch, alg, device, args.steps, hbm_peak, peak_src, peaks,
                                                 ref, cores, traffic_db))
-            configs.append(lattice_model_config(pkg, dev, shapes, "gpt2", device, args.steps, hbm_peak, peak_src, peaks, ref, cores))
+            configs.append(lattice_model_config(pkg, dev, shapes, "gpt2", device, args.steps, hbm_peak, peak_src, peaks, ref, cores, traffic_db))
             # GPT2-XL: GPU time only (the reference's LATTICE pass over 6.55 GB takes ~20 s; parity at full size is in tests/)
             configs.append(lattice_model_config(pkg, dev, shapes, "gpt2-xl", device, args.steps, hbm_peak, peak_src, peaks, None, cores))
         cifar, _ = dataset_config("cifar10_shaped", "CIFAR10-shaped synthetic dataset (50,000 x 3,072 B uint8, 16 sources) LtHash",
                                   cifar_shaped(np), np, torch, dsm, dev, dd, world, rank, args.steps, args.warmup, barrier,
-                                  device, hbm_peak, peak_src, peaks, ref, cores)
+                                  device, hbm_peak, peak_src, peaks, ref, cores, traffic_db)
         configs.append(cifar)
         pool_arrays = hellaswag_shaped(np)
         pool, (pdig, pcounts) = dataset_config(
             "hellaswag_shaped_pool", "hellaswag-shaped token arrays (40,000 ragged samples, 16 curators) LtHash", pool_arrays,
-            np, torch, dsm, dev, dd, world, rank, args.steps, args.warmup, barrier, device, hbm_peak, peak_src, peaks, ref, cores)
+            np, torch, dsm, dev, dd, world, rank, args.steps, args.warmup, barrier, device, hbm_peak, peak_src, peaks, ref, cores,
+            traffic_db)
         if rank == 0:
             # config 5 end to end: one signed bundle per curator + one for the GPT2-XL root, then verification
             n_cur = pool_arrays[5]

@@ -12,7 +12,7 @@ import torch
 sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 from paper_2510_00554_b200 import _native, dataset as dsm, device as dev  # noqa: E402
 
-reps = int(sys.argv[1]) if len(sys.argv) > 1 else 20
+reps = int(sys.argv[1]) if len(sys.argv) > 1 and sys.argv[1].isdigit() else 20
 lib = _native.load()
 
 
@@ -51,42 +51,47 @@ def ragged(n, seed):
     return tokens.view(np.uint8), offsets, lengths, np.arange(n, dtype=np.uint64), r3.choice(n_cur, size=n, p=r3.dirichlet(np.ones(n_cur))), n_cur
 
 
-only = os.environ.get("PROBE_ONLY", "").split(":") if os.environ.get("PROBE_ONLY") else None   # e.g. ragged_2M:lanes_w12
-out = {}
-for name, make in (("cifar10_shaped", cifar), ("hellaswag_40k", lambda: ragged(40_000, 2)), ("ragged_2M", lambda: ragged(2_000_000, 5))):
-    if only and name != only[0]:
-        continue
-    shard, offs, lens, ids, src, n_src = make()
-    ds = dsm.DeviceDataset.from_host(shard, offs, lens, ids, src, list(range(n_src)))
-    acc = dev.LatticeAccumulator(n_src)
-    variants = [("grid", _native.SCHEDULE_GRID, None), ("chains", _native.SCHEDULE_FUSED, None)]
-    variants += [(f"lanes_w{w}", _native.SCHEDULE_PERSISTENT, w) for w in (8, 12, 16)]
-    variants += [("lanes_auto", _native.SCHEDULE_PERSISTENT, 0)]
-    ref = None
-    for vname, sched, w in variants:
-        if only and len(only) > 1 and vname not in (only[1], "grid"):
+def main():
+    only = os.environ.get("PROBE_ONLY", "").split(":") if os.environ.get("PROBE_ONLY") else None   # e.g. ragged_2M:lanes_w12
+    out = {}
+    for name, make in (("cifar10_shaped", cifar), ("hellaswag_40k", lambda: ragged(40_000, 2)), ("ragged_2M", lambda: ragged(2_000_000, 5))):
+        if only and name != only[0]:
             continue
-        lib.snt_merkle_schedule(sched)
-        if w:
-            os.environ["SNT_LT_LANES_WARPS"] = str(w)
-        else:
-            os.environ.pop("SNT_LT_LANES_WARPS", None)
-        acc.zero_()
-        dig = torch.zeros(ds.n_samples * 64, dtype=torch.uint8, device="cuda")
-        ds.accumulate(acc, digests=dig)
-        got = (acc.digests(), bytes(dig.cpu().numpy().tobytes()))
-        if ref is None:
-            ref = got
-        ok = got == ref
-        ms = timed(lambda: ds.accumulate(acc))
-        out[f"{name}_{vname}_us"] = round(ms * 1e3, 1)
-        if not ok:
-            out[f"{name}_{vname}_MISMATCH"] = True
-    if name == "ragged_2M":
-        lib.snt_merkle_schedule(_native.SCHEDULE_GRID)
-        dss = ds.sorted_by_length()
-        out["ragged_2M_sorted_grid_us"] = round(timed(lambda: dss.accumulate(acc)) * 1e3, 1)
-    lib.snt_merkle_schedule(_native.SCHEDULE_PERSISTENT)
-    os.environ.pop("SNT_LT_LANES_WARPS", None)
-    del ds, acc
-print(json.dumps(out))
+        shard, offs, lens, ids, src, n_src = make()
+        ds = dsm.DeviceDataset.from_host(shard, offs, lens, ids, src, list(range(n_src)))
+        acc = dev.LatticeAccumulator(n_src)
+        variants = [("grid", _native.SCHEDULE_GRID, None), ("chains", _native.SCHEDULE_FUSED, None)]
+        variants += [(f"lanes_w{w}", _native.SCHEDULE_PERSISTENT, w) for w in (8, 12, 16)]
+        variants += [("lanes_auto", _native.SCHEDULE_PERSISTENT, 0)]
+        ref = None
+        for vname, sched, w in variants:
+            if only and len(only) > 1 and vname not in (only[1], "grid"):
+                continue
+            lib.snt_merkle_schedule(sched)
+            if w:
+                os.environ["SNT_LT_LANES_WARPS"] = str(w)
+            else:
+                os.environ.pop("SNT_LT_LANES_WARPS", None)
+            acc.zero_()
+            dig = torch.zeros(ds.n_samples * 64, dtype=torch.uint8, device="cuda")
+            ds.accumulate(acc, digests=dig)
+            got = (acc.digests(), bytes(dig.cpu().numpy().tobytes()))
+            if ref is None:
+                ref = got
+            ok = got == ref
+            ms = timed(lambda: ds.accumulate(acc))
+            out[f"{name}_{vname}_us"] = round(ms * 1e3, 1)
+            if not ok:
+                out[f"{name}_{vname}_MISMATCH"] = True
+        if name == "ragged_2M":
+            lib.snt_merkle_schedule(_native.SCHEDULE_GRID)
+            dss = ds.sorted_by_length()
+            out["ragged_2M_sorted_grid_us"] = round(timed(lambda: dss.accumulate(acc)) * 1e3, 1)
+        lib.snt_merkle_schedule(_native.SCHEDULE_PERSISTENT)
+        os.environ.pop("SNT_LT_LANES_WARPS", None)
+        del ds, acc
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()
