@@ -773,6 +773,29 @@ def run_ours(args):
                "api": "hash_model(HashConfig(MERKLE, IN_PLACE, SHA256, 8192), TensorMap(pinned host tensors))"}
         del model, host_entries
 
+    # ---- the same call on ORDINARY (pageable) host memory -- numpy arrays, what a state dict loaded on the CPU or the
+    #      reference's load_model hands over: staged through the pinned ring by copy threads (device.RingWriter)
+    e2e_pageable = None
+    if host_pinned and world == 1:
+        pageable, seen_p = [], {}
+        for name, t in sd:
+            key = t.data_ptr()
+            if key not in seen_p:
+                seen_p[key] = np.array(host_pinned[(key, True)].numpy())       # a copy in pageable memory
+            pageable.append((name, seen_p[key]))
+        model_p = pkg.TensorMap(pageable)
+        assert pkg.hash_model(cfg, model_p).model_digest.data.hex() == root_hex, "pageable-host hash_model differs"
+        best = None
+        for _ in range(2):
+            t0 = time.perf_counter()
+            pkg.hash_model(cfg, model_p)
+            dt_p = time.perf_counter() - t0
+            best = dt_p if best is None else min(best, dt_p)
+        e2e_pageable = {"value": round(total_bytes / best / 1e9, 3), "unit": UNIT, "ms_per_step": round(best * 1e3, 3),
+                        "h2d_bytes_per_step": int(total_bytes), "steps": 2,
+                        "api": "hash_model(cfg, TensorMap(numpy arrays in pageable host memory)), host wall clock, best of 2"}
+        del model_p, pageable, seen_p
+
     # ---- CPU baseline on this box's host cores (rank 0, N = 1): the reference package on the SAME bytes,
     #      bit-exactness asserted before anything is printed
     cpu = None
@@ -885,7 +908,7 @@ def run_ours(args):
                        "l2_policy": "inputs (6.55 GB per pass) larger than the 126 MB L2",
                        "root": root_hex, "root_matches_pinned": PINNED_ROOTS.get((args.arch, args.alg), root_hex) == root_hex},
             **({"debug": "ranks share GPU 0 over gloo; not a measurement"} if same_gpu else {}),
-            "e2e": e2e, "api_device_resident": api_resident, "gpu_launches": launches, "clocks": clocks.summary(),
+            "e2e": e2e, "e2e_pageable_host": e2e_pageable, "api_device_resident": api_resident, "gpu_launches": launches, "clocks": clocks.summary(),
             "roofline": roofline, "int_pipe": int_pipe, "cpu_baseline": cpu, "schedules": schedules, "configs": configs,
             # kept for readers of round 1's line: the CIFAR10-shaped entry of `configs`
             "dataset": next((c for c in (configs or []) if c.get("metric", "").startswith("cifar10")), None),

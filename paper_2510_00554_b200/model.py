@@ -333,7 +333,7 @@ def _inplace_merkle_staged(cfg: HashConfig, model: TensorMap, workers: int = 1) 
     Device buffers are allocated up front (the plan needs their addresses): tensors that are already
     on the GPU stay where they are; host tensors are laid out back to back (256-byte aligned) in ONE
     device arena -- pinned ones are copied straight into their slice, pageable ones travel through
-    the pinned staging ring in 32 MB transfers. All copies run on a side
+    the pinned staging ring in 32 MB transfers (``device.RingWriter``). All copies run on a side
     stream; the leaf kernel for a ~256 MB group of whole tensors is enqueued as soon as its bytes
     have landed, and the tree reduction runs once at the end over the leaf digests.
     """
@@ -368,21 +368,8 @@ def _inplace_merkle_staged(cfg: HashConfig, model: TensorMap, workers: int = 1) 
         side = torch.cuda.Stream()
         side.wait_stream(main)
         arena.record_stream(side)            # the arena is filled by copies on the side stream
-        # the staging buffer being filled mirrors the arena range [chunk_base, chunk_base + chunk_fill)
-        slot, chunk_base, chunk_fill, tasks = -1, 0, 0, []
-
-        def flush_chunk():
-            nonlocal slot, chunk_fill, tasks
-            if slot < 0 or chunk_fill == 0:
-                return
-            for t in tasks:
-                t.result()
-            with torch.cuda.stream(side):
-                arena[chunk_base:chunk_base + chunk_fill].copy_(ring.bufs[slot][:chunk_fill], non_blocking=True)
-                ev = torch.cuda.Event()
-                ev.record(side)
-            ring.events[slot] = ev
-            slot, chunk_fill, tasks = -1, 0, []
+        # pageable bytes travel through the staging ring: memcpy tasks queued ahead, transfers issued on `side`
+        writer = _dev.RingWriter(ring, arena, side) if ring is not None else None
 
         first, group_begin, group_bytes = 0, 0, 0
         n = len(dst)
@@ -406,7 +393,8 @@ def _inplace_merkle_staged(cfg: HashConfig, model: TensorMap, workers: int = 1) 
 
         for i, (_, buf) in enumerate(entries):
             if kinds[i] == PINNED and sizes[i]:
-                flush_chunk()        # a ring transfer covers one contiguous arena range: it must not span this slice
+                if writer is not None:
+                    writer.close()   # a ring transfer covers one contiguous arena range: it must not span this slice
                 src_t = buf if buf.is_contiguous() else buf.contiguous()
                 if src_t is not buf and not src_t.is_pinned():
                     flush_pinned()
@@ -420,30 +408,12 @@ def _inplace_merkle_staged(cfg: HashConfig, model: TensorMap, workers: int = 1) 
             elif kinds[i] == PAGEABLE and sizes[i]:
                 flush_pinned()       # keep the arena filling in order on the side stream
                 src = _host_tensor(buf).numpy() if isinstance(buf, torch.Tensor) else _dev.host_bytes_view(buf)
-                pos = 0
-                while pos < sizes[i]:
-                    if slot < 0:
-                        slot, chunk_base = ring.acquire(), arena_off[i] + pos
-                    so = arena_off[i] + pos - chunk_base
-                    if so >= _dev.STAGE_SLOT_BYTES:
-                        flush_chunk()
-                        continue
-                    take = min(sizes[i] - pos, _dev.STAGE_SLOT_BYTES - so)
-                    view = ring.views[slot]
-                    if take < _dev.STAGE_INLINE_MAX_BYTES:            # a task costs more than a small memcpy
-                        np.copyto(view[so:so + take], src[pos:pos + take])
-                    else:
-                        for p0 in range(0, take, _dev.STAGE_PIECE_BYTES):
-                            p1 = min(take, p0 + _dev.STAGE_PIECE_BYTES)
-                            tasks.append(ring.pool.submit(np.copyto, view[so + p0:so + p1], src[pos + p0:pos + p1]))
-                    chunk_fill = so + take
-                    pos += take
-                    if chunk_fill >= _dev.STAGE_SLOT_BYTES:
-                        flush_chunk()
+                writer.write(arena_off[i], src)
             group_bytes += sizes[i]
             first_next = first + -(-sizes[i] // bs)
             if group_bytes >= STAGE_CHUNK_BYTES or i == n - 1:
-                flush_chunk()
+                if writer is not None:
+                    writer.drain()
                 flush_pinned()
                 done = torch.cuda.Event()
                 done.record(side)

@@ -6,7 +6,7 @@ sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 import paper_2510_00554_b200 as pkg
 from paper_2510_00554_b200 import shapes
 out = {}
-for arch in ("gpt2", "bert-large"):
+for arch in (sys.argv[1:] or ("gpt2", "bert-large", "gpt2-xl")):
     rng = np.random.default_rng(0)
     entries = []
     for name, shape, alias in shapes.ARCHITECTURES[arch]():
@@ -17,7 +17,7 @@ for arch in ("gpt2", "bert-large"):
     cfg = pkg.HashConfig(pkg.Construction.MERKLE, pkg.Strategy.IN_PLACE, pkg.CompressionAlg.SHA256)
     out[arch] = {"bytes": model.total_bytes}
     from paper_2510_00554_b200 import device as dv
-    for slot_mb, slots in ((32, 4), (64, 4), (128, 3), (256, 2)):      # transfer size of the staging ring
+    for slot_mb, slots in ((32, 4), (64, 4), (128, 3)):      # transfer size of the staging ring
         dv.STAGE_SLOT_BYTES, dv.STAGE_RING_SLOTS = slot_mb << 20, slots
         pkg.hash_model(cfg, model)
         ts = []
