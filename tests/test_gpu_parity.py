@@ -228,6 +228,33 @@ def test_host_model_staged_in_overlapped_chunks(pkg, corc, monkeypatch):
         assert res.block_count == tl.leaf_count(8192)
 
 
+def test_page_locked_model_copy_first_with_small_tensors_through_the_gather(pkg, corc, monkeypatch):
+    """Every host tensor page-locked (plus CUDA entries): the copy-first path. Tensors below SMALL_H2D_BYTES are
+    fetched by one gather launch straight from the pinned host memory, the others by the copy engine; sizes on both
+    sides of the threshold, empty tensors, odd lengths, several copy/hash groups."""
+    from paper_2510_00554_b200 import model as mm
+
+    monkeypatch.setattr(mm, "STAGE_CHUNK_BYTES", 6 << 20)
+    rng = np.random.default_rng(17)
+    small = mm.SMALL_H2D_BYTES
+    sizes = [17 << 20, 3, 0, small - 1, small, small + 1, (7 << 20) + 13, 6400, 8192, 1, (15 << 20) + 5, 100, 0, 4096 * 3]
+    host = [rng.integers(0, 256, size=s, dtype=np.uint8) for s in sizes]
+    entries = [(f"t{i}", torch.from_numpy(h).cuda() if i in (6, 11) else torch.from_numpy(h).pin_memory())
+               for i, h in enumerate(host)]
+    assert sum(sizes) >= mm.STAGE_PIPELINE_MIN_BYTES
+    taken = []
+    real = mm._inplace_merkle_pinned
+    monkeypatch.setattr(mm, "_inplace_merkle_pinned", lambda cfg, model: taken.append(1) or real(cfg, model))
+    tl = corc.TensorList(host)
+    for name in ALGS:
+        cfg = pkg.HashConfig(pkg.Construction.MERKLE, pkg.Strategy.IN_PLACE, _alg(pkg, name), 8192)
+        for _ in range(2):
+            res = pkg.hash_model(cfg, pkg.TensorMap(entries))
+            assert res.model_digest.data == corc.inplace_merkle(name, tl, 8192, 4), name
+            assert res.block_count == tl.leaf_count(8192)
+    assert len(taken) == 2 * len(ALGS)
+
+
 @pytest.mark.parametrize("slot_kb,piece_kb", [(1024, 256), (768, 1000), (32768, 4096)])
 def test_pageable_inputs_through_the_staging_ring(pkg, corc, monkeypatch, slot_kb, piece_kb):
     """bytes / numpy / unpinned tensors ride the pinned ring: tensors straddle transfers, slots wrap around."""
