@@ -53,6 +53,7 @@ SIGNATURES = {
     "snt_merkle_root": (c_int, [c_int, c_void_p, c_uint64, c_void_p, c_size_t, c_void_p, c_void_p]),
     "snt_lthash_samples": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_uint64, c_uint32,
                                    c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "snt_device_reads_pinned_host": (c_int, []),
     "snt_lthash_samples_shaped": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_uint64, c_uint32,
                                           c_void_p, c_void_p, c_void_p, c_void_p, c_uint32, c_void_p]),
     "snt_lthash_model": (c_int, [c_void_p, c_uint64, c_uint64, c_void_p, c_void_p, c_void_p, c_void_p]),

@@ -782,6 +782,17 @@ int snt_memcpy_h2d_batch(void* const* d_dst, const void* const* h_src, const uin
 
 uint32_t snt_gather_chunk_bytes(void) { return GATHER_CHUNK_BYTES; }
 
+int snt_device_reads_pinned_host(void) {
+    static const int ok = [] {
+        int dev = 0, unified = 0, same_ptr = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+        if (cudaDeviceGetAttribute(&unified, cudaDevAttrUnifiedAddressing, dev) != cudaSuccess) return 0;
+        if (cudaDeviceGetAttribute(&same_ptr, cudaDevAttrCanUseHostPointerForRegisteredMem, dev) != cudaSuccess) return 0;
+        return (unified && same_ptr) ? 1 : 0;
+    }();
+    return ok;
+}
+
 int snt_gather_spans(const uint64_t* d_src_addr, const uint64_t* d_len, const uint64_t* d_dst_off,
                      const uint64_t* d_chunk_first, uint32_t n_spans, uint64_t n_chunks,
                      uint32_t pad_block, void* d_dst, snt_stream_t stream) {

@@ -255,6 +255,7 @@ def _inplace_merkle_pinned(cfg: HashConfig, model: TensorMap) -> Optional[ModelD
     small_len: List[int] = []
     small_off: List[int] = []
     in_arena = [False] * n
+    small_limit = SMALL_H2D_BYTES if _dev._native.load().snt_device_reads_pinned_host() else 0
     for i, (_, buf) in enumerate(entries):
         if not isinstance(buf, torch.Tensor) or not buf.is_contiguous():
             return None
@@ -266,7 +267,7 @@ def _inplace_merkle_pinned(cfg: HashConfig, model: TensorMap) -> Optional[ModelD
             if nbytes == 0:
                 continue                                # owns no leaves, needs no address
             in_arena[i] = True
-            if nbytes < SMALL_H2D_BYTES:
+            if nbytes < small_limit:
                 small_src.append(buf.data_ptr())
                 small_len.append(nbytes)
                 small_off.append(arena_total)

@@ -100,9 +100,15 @@ int hc_blake2b_sliced(int T, uint64_t tag0, uint64_t tag1, const uint8_t* p, uin
     for (uint64_t b = 0; b < n; b += slice) {
         uint64_t bufs[2 * B2S_SLOTS];
         memset(bufs, 0x5A, sizeof(bufs));        // a fresh thread's staging buffers: nothing may be carried in them
-        if (T == 0) Blake2bStaged<1>::hash_blocks<0>(bufs, tag0, tag1, p, len, b, b + slice, h);
-        else if (T == 1) Blake2bStaged<1>::hash_blocks<1>(bufs, tag0, tag1, p, len, b, b + slice, h);
-        else Blake2bStaged<1>::hash_blocks<2>(bufs, tag0, tag1, p, len, b, b + slice, h);
+        // odd slices through the compress-from-the-staging-buffer form (ROLLED; on the host its rounds are the unrolled
+        // ones, what differs is that the carried words are moved before the block is compressed)
+        const bool rolled = (b / slice) & 1;
+        if (T == 0) rolled ? Blake2bStaged<1>::hash_blocks<0, true>(bufs, tag0, tag1, p, len, b, b + slice, h)
+                           : Blake2bStaged<1>::hash_blocks<0>(bufs, tag0, tag1, p, len, b, b + slice, h);
+        else if (T == 1) rolled ? Blake2bStaged<1>::hash_blocks<1, true>(bufs, tag0, tag1, p, len, b, b + slice, h)
+                                : Blake2bStaged<1>::hash_blocks<1>(bufs, tag0, tag1, p, len, b, b + slice, h);
+        else rolled ? Blake2bStaged<1>::hash_blocks<2, true>(bufs, tag0, tag1, p, len, b, b + slice, h)
+                    : Blake2bStaged<1>::hash_blocks<2>(bufs, tag0, tag1, p, len, b, b + slice, h);
     }
     memcpy(out, h, 64);
     return 0;
