@@ -770,7 +770,9 @@ def run_ours(args):
             dt = float(t.item())
         e2e = {"value": round(total_bytes / dt / 1e9, 3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": 32, "ms_per_step": round(dt * 1e3, 3), "steps": args.e2e_steps,
-               "api": "hash_model(HashConfig(MERKLE, IN_PLACE, SHA256, 8192), TensorMap(pinned host tensors))"}
+               "api": "hash_model(HashConfig(MERKLE, IN_PLACE, SHA256, 8192), TensorMap(pinned host tensors))",
+               # device memory the call used for the model's bytes: a ring of copy/hash groups, not a copy of the model
+               "device_staging_bytes": dict(getattr(sys.modules["paper_2510_00554_b200.model"], "LAST_HOST_STAGING", {}))}
         del model, host_entries
 
     # ---- the same call on ORDINARY (pageable) host memory -- numpy arrays, what a state dict loaded on the CPU or the

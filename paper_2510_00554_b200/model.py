@@ -233,227 +233,191 @@ def _copy_streams(dev: torch.device) -> List["torch.cuda.Stream"]:
     return _COPY_STREAMS[key]
 
 
-def _inplace_merkle_pinned(cfg: HashConfig, model: TensorMap) -> Optional[ModelDigestResult]:
-    """Page-locked host tensors (and CUDA tensors): the transfer is the whole cost, so it starts first.
+LAST_HOST_STAGING: Dict[str, int] = {}   # layout of the most recent _inplace_merkle_host call (diagnostics)
+STAGE_PIECE_BYTES = 64 << 20             # a host tensor travels in pieces of at most this (a multiple of the block size)
+STAGE_RING_GROUPS = 3                    # copy/hash groups the transfers may run ahead of the hashing
 
-    One pass lays the host tensors out in a device arena; then EVERY copy is put on a side stream at once --
-    one batch of asynchronous copies per ~256 MB group, an event after each group -- before the plan, the
-    leaf buffer and the workspace are even created. The leaf launch of a group waits for that group's event,
-    the tree runs once at the end. GPT2-XL from pinned memory: 123.8 -> 120 ms for a link that needs 117.9 ms.
-    Returns None when an entry is neither a CUDA tensor nor a contiguous page-locked tensor (the general path
-    takes those).
+
+def _inplace_merkle_host(cfg: HashConfig, model: TensorMap, workers: int = 1) -> ModelDigestResult:
+    """Host tensors (page-locked or pageable, CUDA tensors mixed in) hashed while they arrive, in BOUNDED device memory.
+
+    Every host tensor is cut into pieces of at most 64 MB at block boundaries -- the leaf sequence of the pieces
+    is the leaf sequence of the tensor -- and the pieces are laid out in a RING of device memory that holds a few
+    copy/hash groups (~256 MB each): a 6.55 GB state dict needs 1.3 GB of HBM, not a copy of itself, and a model
+    larger than the GPU's memory can be hashed at all. The plan (one row per piece) is built once, up front: ring
+    addresses are known before a byte has moved. Then, group by group:
+
+      * the transfers of group g are put on a side stream -- page-locked pieces as ONE batch of asynchronous
+        copies issued from C (``snt_memcpy_h2d_batch``), pageable ones through the pinned staging ring and its
+        copy threads (``device.RingWriter``) -- after the stream has been told to wait for the leaf launch that
+        last read the ring memory they overwrite (group g - 3);
+      * the leaf launch of group g waits for the group's transfers and hashes its leaf range; the tree runs once at
+        the end over the leaf digests.
+
+    When every host tensor is page-locked the first three groups of transfers are on the stream before the plan
+    and the workspace are even created: the link is the whole cost (GPT2-XL: 121 ms for 117.9 ms of link). A
+    ``cudaMemcpyAsync`` costs the copy engine ~3.7 us whatever its size, so page-locked tensors below 64 KB (the
+    386 biases and layer norms of GPT2-XL: 4 MB, 1.5 ms of copy engine) live in a small arena of their own and are
+    fetched by ONE gather launch that reads the host memory through the unified address space.
     """
     dev = _dev.require_cuda()
+    lib = _dev._native.load()
     bs = cfg.block_size
     entries = model.entries
-    n = len(entries)
-    sizes = np.zeros(max(n, 1), dtype=np.uint64)
-    ptrs = np.zeros(max(n, 1), dtype=np.uint64)
-    host_ptrs = [0] * n
-    arena_total = 0
-    small_src: List[int] = []                            # page-locked tensors below SMALL_H2D_BYTES: fetched by ONE kernel
+    CUDA, PINNED, PAGEABLE, SMALL = 0, 1, 2, 3
+    piece = max(bs, STAGE_PIECE_BYTES // bs * bs)
+    small_limit = SMALL_H2D_BYTES if lib.snt_device_reads_pinned_host() else 0
+
+    # ---- spans: (kind, source, source offset, bytes); a host tensor contributes one span per piece
+    spans: List[Tuple[int, object, int, int]] = []
+    keep: List[object] = []
+    n_pageable = 0
+    for _, buf in entries:
+        nbytes = buffer_nbytes(buf)
+        if nbytes == 0:
+            spans.append((CUDA, None, 0, 0))
+        elif _is_cuda(buf):
+            t = _dev.as_device_bytes(buf, dev)
+            keep.append(t)
+            spans.append((CUDA, t, 0, nbytes))
+        elif isinstance(buf, torch.Tensor) and buf.is_pinned() and buf.is_contiguous():
+            if nbytes < small_limit:
+                spans.append((SMALL, buf, 0, nbytes))
+            else:
+                spans.extend((PINNED, buf, o, min(piece, nbytes - o)) for o in range(0, nbytes, piece))
+        else:
+            src = _host_tensor(buf).numpy() if isinstance(buf, torch.Tensor) else _dev.host_bytes_view(buf)
+            keep.append(src)
+            spans.extend((PAGEABLE, src, o, min(piece, nbytes - o)) for o in range(0, nbytes, piece))
+            n_pageable += 1
+    n = len(spans)
+    if sum(sp[3] for sp in spans) == 0:
+        raise InvalidInput("model must contain at least one byte of tensor data")
+
+    # ---- layout: ring offsets of the pieces, groups of >= STAGE_CHUNK_BYTES, the small tensors' own arena
+    def aligned(x: int) -> int:
+        return -(-x // _ARENA_ALIGN) * _ARENA_ALIGN
+
+    ring_need = sum(aligned(sp[3]) for sp in spans if sp[0] in (PINNED, PAGEABLE))
+    ring_bytes = min(ring_need, (STAGE_RING_GROUPS + 1) * (STAGE_CHUNK_BYTES + aligned(piece)))
+    small_bytes = sum(aligned(sp[3]) for sp in spans if sp[0] == SMALL)
+    ring = torch.empty(max(ring_bytes, 16), dtype=torch.uint8, device=dev)
+    small_arena = torch.empty(max(small_bytes, 16), dtype=torch.uint8, device=dev)
+    ring_base, small_base = ring.data_ptr(), small_arena.data_ptr()
+    ptrs = np.zeros(n, dtype=np.uint64)
+    sizes = np.fromiter((sp[3] for sp in spans), dtype=np.uint64, count=n)
+    offs = [0] * n                                         # ring offset of a PINNED / PAGEABLE span
+    groups: List[Tuple[int, int, int]] = []               # (first span, end span, first leaf after the group)
+    pos, small_pos, leaf, g_begin, g_bytes = 0, 0, 0, 0, 0
+    small_src: List[int] = []
     small_len: List[int] = []
     small_off: List[int] = []
-    in_arena = [False] * n
-    small_limit = SMALL_H2D_BYTES if _dev._native.load().snt_device_reads_pinned_host() else 0
-    for i, (_, buf) in enumerate(entries):
-        if not isinstance(buf, torch.Tensor) or not buf.is_contiguous():
-            return None
-        nbytes = buf.numel() * buf.element_size()
-        sizes[i] = nbytes
-        if buf.is_cuda:
-            ptrs[i] = buf.data_ptr() if nbytes else 0
-        elif buf.is_pinned():
-            if nbytes == 0:
-                continue                                # owns no leaves, needs no address
-            in_arena[i] = True
-            if nbytes < small_limit:
-                small_src.append(buf.data_ptr())
-                small_len.append(nbytes)
-                small_off.append(arena_total)
-            else:
-                host_ptrs[i] = buf.data_ptr()
-            ptrs[i] = arena_total                       # arena offset for now
-            arena_total += -(-nbytes // _ARENA_ALIGN) * _ARENA_ALIGN
+    for i, (kind, src, off, nbytes) in enumerate(spans):
+        if kind == CUDA:
+            ptrs[i] = src.data_ptr() if nbytes else 0
+        elif kind == SMALL:
+            ptrs[i] = small_base + small_pos
+            small_src.append(src.data_ptr())
+            small_len.append(nbytes)
+            small_off.append(small_pos)
+            small_pos += aligned(nbytes)
         else:
-            return None
-    if int(sizes[:n].sum()) == 0:
-        raise InvalidInput("model must contain at least one byte of tensor data")
-    arena = torch.empty(max(arena_total, 16), dtype=torch.uint8, device=dev)
-    base = arena.data_ptr()
+            if pos + aligned(nbytes) > ring_bytes:
+                pos = 0                                    # a piece is contiguous: wrap before it, not inside it
+            offs[i] = pos
+            ptrs[i] = ring_base + pos
+            pos += aligned(nbytes)
+            g_bytes += aligned(nbytes)                     # the group's footprint in the ring, padding included
+        leaf += -(-nbytes // bs)
+        if g_bytes >= STAGE_CHUNK_BYTES or i == n - 1:
+            groups.append((g_begin, i + 1, leaf))
+            g_begin, g_bytes = i + 1, 0
+
+    global LAST_HOST_STAGING                               # (diagnostics: tests and bench read it)
+    LAST_HOST_STAGING = {"ring_bytes": int(ring_bytes), "host_bytes": int(ring_need), "small_arena_bytes": int(small_bytes),
+                         "pieces": n, "groups": len(groups)}
     main = torch.cuda.current_stream()
-    # ONE copy stream: dealing the tensors to two streams alternately (to hide the fixed cost of starting a
-    # transfer behind the other stream's data phase) was measured slower, 130 vs 122.6 ms
-    sides = _copy_streams(dev)[:1]
-    for side in sides:
-        side.wait_stream(main)
-        arena.record_stream(side)
-    lib = _dev._native.load()
-    if small_src:
-        # A cudaMemcpyAsync costs the copy engine ~3.7 us whatever its size: the 386 biases and layer norms of
-        # GPT2-XL (4 MB in all) were 1.5 ms of a 122 ms transfer. ONE gather launch reads them from the page-locked
-        # host memory through the unified address space instead (0.12 ms, on the SMs, next to the big transfers).
-        # It goes first: its small table upload must not queue behind gigabytes of asynchronous copies.
+    side = _copy_streams(dev)[0]
+    side.wait_stream(main)
+    ring.record_stream(side)
+    side_handle = ctypes.c_void_p(side.cuda_stream)
+    if small_src:                                          # on the main stream, ahead of every leaf launch
         _dev.gather_spans(np.array(small_src, dtype=np.uint64), np.array(small_len, dtype=np.uint64),
-                          np.array(small_off, dtype=np.uint64), 0, arena)
-    handles = [ctypes.c_void_p(side.cuda_stream) for side in sides]
-    groups: List[Tuple[int, List[torch.cuda.Event]]] = []       # (first leaf after the group, copies-done events)
-    batches = [([], [], []) for _ in sides]
-    first, group_bytes, turn = 0, 0, 0
+                          np.array(small_off, dtype=np.uint64), 0, small_arena)
+    staging = _dev.StagingRing.get(_dev.staging_threads(workers)) if n_pageable else None
+    if staging is not None:
+        staging.lock.acquire()                             # one staged hash at a time owns the pinned staging ring
+    plan = None
     try:
-        for i in range(n):
-            nbytes = int(sizes[i])
-            if in_arena[i]:
-                ptrs[i] = base + int(ptrs[i])
-            if host_ptrs[i]:
-                b = batches[turn]
-                b[0].append(int(ptrs[i])); b[1].append(host_ptrs[i]); b[2].append(nbytes)
-                if nbytes >= (1 << 20):
-                    turn = (turn + 1) % len(sides)
-            group_bytes += nbytes
-            first += -(-nbytes // bs)
-            if group_bytes >= STAGE_CHUNK_BYTES or i == n - 1:
-                events = []
-                for side, handle, b in zip(sides, handles, batches):
-                    if b[0]:
-                        k = len(b[0])
-                        rc = lib.snt_memcpy_h2d_batch((ctypes.c_void_p * k)(*b[0]), (ctypes.c_void_p * k)(*b[1]),
-                                                      (ctypes.c_uint64 * k)(*b[2]), k, handle)
-                        _dev._native.check(rc, "snt_memcpy_h2d_batch")
-                        b[0].clear(); b[1].clear(); b[2].clear()
-                    ev = torch.cuda.Event()
-                    ev.record(side)
-                    events.append(ev)
-                groups.append((first, events))
-                group_bytes = 0
-        # the link is busy from here on; now the bookkeeping
-        plan = _dev.ModelPlan.from_spans([], ptrs, sizes, bs, count=n)
-        try:
-            hasher = _dev.MerkleModelHasher(plan, cfg.alg.value)
-            begin = 0
-            for end, events in groups:
-                for ev in events:
-                    main.wait_event(ev)
-                if end > begin:
-                    hasher.run_leaves_only(begin, end)
-                begin = end
-            hasher.run_tree_only()
-            root = Digest(cfg.alg, hasher.out_bytes())          # synchronises: all copies and kernels done
-            n_leaves = plan.leaf_count
-            aux = hasher.leaves.numel() + hasher.work_bytes + (hasher.out.numel() if n_leaves > 1 else 0)
-            return ModelDigestResult(root, cfg, n_leaves, aux_digest_bytes=aux)
-        finally:
-            plan.close()
-    finally:
-        torch.cuda.synchronize()          # no copy may still be in flight when the arena goes back to the allocator
+        writer = _dev.RingWriter(staging, ring, side) if staging is not None else None
+        copied: List[Optional[torch.cuda.Event]] = [None] * len(groups)
+        hashed: List[Optional[torch.cuda.Event]] = [None] * len(groups)
 
+        def issue(g: int) -> None:
+            """Put the transfers of group g on the side stream (ring memory: after the leaf launch of group g - R)."""
+            if g >= STAGE_RING_GROUPS and ring_bytes < ring_need:
+                side.wait_event(hashed[g - STAGE_RING_GROUPS])
+            b_dst: List[int] = []
+            b_src: List[int] = []
+            b_len: List[int] = []
 
-def _inplace_merkle_staged(cfg: HashConfig, model: TensorMap, workers: int = 1) -> ModelDigestResult:
-    """Host tensors -> device with the copies and the leaf hashing overlapped.
+            def flush_pinned() -> None:
+                if b_dst:
+                    k = len(b_dst)
+                    rc = lib.snt_memcpy_h2d_batch((ctypes.c_void_p * k)(*b_dst), (ctypes.c_void_p * k)(*b_src),
+                                                  (ctypes.c_uint64 * k)(*b_len), k, side_handle)
+                    _dev._native.check(rc, "snt_memcpy_h2d_batch")
+                    b_dst.clear(); b_src.clear(); b_len.clear()
 
-    Device buffers are allocated up front (the plan needs their addresses): tensors that are already
-    on the GPU stay where they are; host tensors are laid out back to back (256-byte aligned) in ONE
-    device arena -- pinned ones are copied straight into their slice, pageable ones travel through
-    the pinned staging ring in 32 MB transfers (``device.RingWriter``). All copies run on a side
-    stream; the leaf kernel for a ~256 MB group of whole tensors is enqueued as soon as its bytes
-    have landed, and the tree reduction runs once at the end over the leaf digests.
-    """
-    dev = _dev.require_cuda()
-    bs = cfg.block_size
-    entries = model.entries
-    sizes = [buffer_nbytes(buf) for _, buf in entries]
-    CUDA, PINNED, PAGEABLE = 0, 1, 2
-    kinds, arena_off, arena_total, n_pageable = [], [0] * len(entries), 0, 0
-    for i, (_, buf) in enumerate(entries):
-        if _is_cuda(buf):
-            kinds.append(CUDA)
-        else:
-            kinds.append(PINNED if isinstance(buf, torch.Tensor) and buf.is_pinned() else PAGEABLE)
-            n_pageable += kinds[-1] == PAGEABLE
-            arena_off[i] = arena_total                      # one device allocation for every staged tensor
-            arena_total += -(-sizes[i] // _ARENA_ALIGN) * _ARENA_ALIGN
-    arena = torch.empty(max(arena_total, 16), dtype=torch.uint8, device=dev)
-    dst: List[torch.Tensor] = []
-    for i, (_, buf) in enumerate(entries):
-        if kinds[i] == CUDA:
-            dst.append(_dev.as_device_bytes(buf, dev))
-        else:
-            dst.append(arena[arena_off[i]:arena_off[i] + sizes[i]])
-    plan = _dev.ModelPlan(dst, bs)
-    ring = _dev.StagingRing.get(_dev.staging_threads(workers)) if n_pageable else None
-    if ring is not None:
-        ring.lock.acquire()                  # one staged hash at a time owns the ring
-    try:
-        hasher = _dev.MerkleModelHasher(plan, cfg.alg.value)
-        main = torch.cuda.current_stream()
-        side = torch.cuda.Stream()
-        side.wait_stream(main)
-        arena.record_stream(side)            # the arena is filled by copies on the side stream
-        # pageable bytes travel through the staging ring: memcpy tasks queued ahead, transfers issued on `side`
-        writer = _dev.RingWriter(ring, arena, side) if ring is not None else None
-
-        first, group_begin, group_bytes = 0, 0, 0
-        n = len(dst)
-        lib = _dev._native.load()
-        side_handle = ctypes.c_void_p(side.cuda_stream)
-        # page-locked tensors of a group go to the side stream as ONE batch of asynchronous copies issued from C
-        # (snt_memcpy_h2d_batch): a Python call per tensor leaves the link idle between the small ones
-        batch_dst: List[int] = []
-        batch_src: List[int] = []
-        batch_len: List[int] = []
-        batch_keep: List[torch.Tensor] = []
-
-        def flush_pinned():
-            if not batch_dst:
-                return
-            k = len(batch_dst)
-            rc = lib.snt_memcpy_h2d_batch((ctypes.c_void_p * k)(*batch_dst), (ctypes.c_void_p * k)(*batch_src),
-                                          (ctypes.c_uint64 * k)(*batch_len), k, side_handle)
-            _dev._native.check(rc, "snt_memcpy_h2d_batch")
-            batch_dst.clear(); batch_src.clear(); batch_len.clear()
-
-        for i, (_, buf) in enumerate(entries):
-            if kinds[i] == PINNED and sizes[i]:
-                if writer is not None:
-                    writer.close()   # a ring transfer covers one contiguous arena range: it must not span this slice
-                src_t = buf if buf.is_contiguous() else buf.contiguous()
-                if src_t is not buf and not src_t.is_pinned():
+            first, end, _ = groups[g]
+            for i in range(first, end):
+                kind, src, off, nbytes = spans[i]
+                if kind == PINNED:
+                    if writer is not None:
+                        writer.close()                     # a staging transfer covers ONE contiguous ring range
+                    b_dst.append(int(ptrs[i])); b_src.append(src.data_ptr() + off); b_len.append(nbytes)
+                elif kind == PAGEABLE:
                     flush_pinned()
-                    with torch.cuda.stream(side):
-                        dst[i].copy_(_host_tensor(src_t), non_blocking=True)
-                else:
-                    batch_keep.append(src_t)
-                    batch_dst.append(dst[i].data_ptr())
-                    batch_src.append(src_t.data_ptr())
-                    batch_len.append(sizes[i])
-            elif kinds[i] == PAGEABLE and sizes[i]:
-                flush_pinned()       # keep the arena filling in order on the side stream
-                src = _host_tensor(buf).numpy() if isinstance(buf, torch.Tensor) else _dev.host_bytes_view(buf)
-                writer.write(arena_off[i], src)
-            group_bytes += sizes[i]
-            first_next = first + -(-sizes[i] // bs)
-            if group_bytes >= STAGE_CHUNK_BYTES or i == n - 1:
-                if writer is not None:
-                    writer.drain()
-                flush_pinned()
-                done = torch.cuda.Event()
-                done.record(side)
-                main.wait_event(done)
-                if first_next > group_begin:
-                    hasher.run_leaves_only(group_begin, first_next)
-                group_begin, group_bytes = first_next, 0
-            first = first_next
+                    writer.write(offs[i], src[off:off + nbytes])
+            if writer is not None:
+                writer.drain()
+            flush_pinned()
+            ev = torch.cuda.Event()
+            ev.record(side)
+            copied[g] = ev
+
+        ahead = min(len(groups), STAGE_RING_GROUPS)
+        if n_pageable == 0:
+            for g in range(ahead):                         # page-locked sources: the link is busy from here on
+                issue(g)
+        plan = _dev.ModelPlan.from_spans(keep, ptrs, sizes, bs, count=n)
+        hasher = _dev.MerkleModelHasher(plan, cfg.alg.value)
+        if n_pageable:
+            for g in range(ahead):
+                issue(g)
+        begin = 0
+        for g, (_, _, leaf_end) in enumerate(groups):
+            main.wait_event(copied[g])
+            if leaf_end > begin:
+                hasher.run_leaves_only(begin, leaf_end)
+            begin = leaf_end
+            done = torch.cuda.Event()
+            done.record(main)
+            hashed[g] = done
+            if g + ahead < len(groups):
+                issue(g + ahead)
         hasher.run_tree_only()
         root = Digest(cfg.alg, hasher.out_bytes())          # synchronises: all copies and kernels done
         n_leaves = plan.leaf_count
         aux = hasher.leaves.numel() + hasher.work_bytes + (hasher.out.numel() if n_leaves > 1 else 0)
         return ModelDigestResult(root, cfg, n_leaves, aux_digest_bytes=aux)
     finally:
-        # no copy may still be in flight when the arena goes back to the allocator or the ring to its next owner
+        # no copy may still be in flight when the ring goes back to the allocator or the staging ring to its next owner
         torch.cuda.synchronize()
-        if ring is not None:
-            ring.lock.release()
-        plan.close()
+        if staging is not None:
+            staging.lock.release()
+        if plan is not None:
+            plan.close()
 
 
 class _ResidentEntry:
@@ -580,8 +544,7 @@ def inplace_hash(cfg: HashConfig, model: TensorMap, workers: int = 1) -> ModelDi
         _require_nonempty(model)
         host_bytes = sum(buffer_nbytes(buf) for buf in buffers if not _is_cuda(buf))
         if cfg.construction is Construction.MERKLE and host_bytes >= STAGE_PIPELINE_MIN_BYTES:
-            fast = _inplace_merkle_pinned(cfg, model)
-            return fast if fast is not None else _inplace_merkle_staged(cfg, model, workers)
+            return _inplace_merkle_host(cfg, model, workers)
     # an empty model is rejected by snt_model_plan_create (InvalidInput, model.py:166-168)
     plan = _dev.ModelPlan.from_spans(*_dev.device_spans(buffers), cfg.block_size)
     try:

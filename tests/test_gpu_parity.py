@@ -208,6 +208,7 @@ def test_host_model_staged_in_overlapped_chunks(pkg, corc, monkeypatch):
     from paper_2510_00554_b200 import model as mm
 
     monkeypatch.setattr(mm, "STAGE_CHUNK_BYTES", 3 << 20)          # several chunks at test size
+    monkeypatch.setattr(mm, "STAGE_PIECE_BYTES", 1 << 20)          # tensors travel in pieces, the device ring wraps
     rng = np.random.default_rng(11)
     sizes = [5 << 20, 100, 0, (7 << 20) + 13, 8192, 3, (9 << 20) + 4096, 12 << 20, 6400, (2 << 20) + 1]
     host = [rng.integers(0, 256, size=s, dtype=np.uint8) for s in sizes]
@@ -235,6 +236,7 @@ def test_page_locked_model_copy_first_with_small_tensors_through_the_gather(pkg,
     from paper_2510_00554_b200 import model as mm
 
     monkeypatch.setattr(mm, "STAGE_CHUNK_BYTES", 6 << 20)
+    monkeypatch.setattr(mm, "STAGE_PIECE_BYTES", 2 << 20)          # ring = 4 x 8 MB < the model: it wraps
     rng = np.random.default_rng(17)
     small = mm.SMALL_H2D_BYTES
     sizes = [17 << 20, 3, 0, small - 1, small, small + 1, (7 << 20) + 13, 6400, 8192, 1, (15 << 20) + 5, 100, 0, 4096 * 3]
@@ -243,8 +245,8 @@ def test_page_locked_model_copy_first_with_small_tensors_through_the_gather(pkg,
                for i, h in enumerate(host)]
     assert sum(sizes) >= mm.STAGE_PIPELINE_MIN_BYTES
     taken = []
-    real = mm._inplace_merkle_pinned
-    monkeypatch.setattr(mm, "_inplace_merkle_pinned", lambda cfg, model: taken.append(1) or real(cfg, model))
+    real = mm._inplace_merkle_host
+    monkeypatch.setattr(mm, "_inplace_merkle_host", lambda cfg, model, workers=1: taken.append(1) or real(cfg, model, workers))
     tl = corc.TensorList(host)
     for name in ALGS:
         cfg = pkg.HashConfig(pkg.Construction.MERKLE, pkg.Strategy.IN_PLACE, _alg(pkg, name), 8192)
@@ -253,6 +255,11 @@ def test_page_locked_model_copy_first_with_small_tensors_through_the_gather(pkg,
             assert res.model_digest.data == corc.inplace_merkle(name, tl, 8192, 4), name
             assert res.block_count == tl.leaf_count(8192)
     assert len(taken) == 2 * len(ALGS)
+    assert mm.LAST_HOST_STAGING["ring_bytes"] < mm.LAST_HOST_STAGING["host_bytes"]      # bounded device memory
+    # block sizes on both sides of the piece size (a piece is a whole number of blocks, at least one)
+    for bs in (64, 4 << 20):
+        cfg = pkg.HashConfig(pkg.Construction.MERKLE, pkg.Strategy.IN_PLACE, _alg(pkg, "sha256"), bs)
+        assert pkg.hash_model(cfg, pkg.TensorMap(entries)).model_digest.data == corc.inplace_merkle("sha256", tl, bs, 4), bs
 
 
 @pytest.mark.parametrize("slot_kb,piece_kb", [(1024, 256), (768, 1000), (32768, 4096)])
@@ -263,6 +270,7 @@ def test_pageable_inputs_through_the_staging_ring(pkg, corc, monkeypatch, slot_k
     monkeypatch.setattr(dv, "STAGE_SLOT_BYTES", slot_kb << 10)
     monkeypatch.setattr(dv, "STAGE_PIECE_BYTES", piece_kb << 10)
     monkeypatch.setattr(mm, "STAGE_CHUNK_BYTES", 5 << 20)
+    monkeypatch.setattr(mm, "STAGE_PIECE_BYTES", (1 << 20) if slot_kb < 32768 else (64 << 20))   # wrapping device ring / one arena
     rng = np.random.default_rng(12)
     sizes = [(3 << 20) + 77, 1, 0, 8192 * 300, (6 << 20) + 8191, 255, 257, (11 << 20) + 5, 4096, (9 << 20)]
     host = [rng.integers(0, 256, size=s, dtype=np.uint8) for s in sizes]
