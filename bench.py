@@ -764,6 +764,12 @@ def run_ours(args):
             e2e_step()
         barrier()
         dt = (time.perf_counter() - t0) / args.e2e_steps
+        torch.cuda.synchronize()                       # one more, untimed call: the device memory the call itself allocates
+        torch.cuda.empty_cache()
+        mem_before = torch.cuda.memory_allocated()
+        torch.cuda.reset_peak_memory_stats()
+        e2e_step()
+        e2e_peak_extra = int(torch.cuda.max_memory_allocated() - mem_before)
         if world > 1:
             t = torch.tensor([dt], device=device)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -772,7 +778,8 @@ def run_ours(args):
                "d2h_bytes_per_step": 32, "ms_per_step": round(dt * 1e3, 3), "steps": args.e2e_steps,
                "api": "hash_model(HashConfig(MERKLE, IN_PLACE, SHA256, 8192), TensorMap(pinned host tensors))",
                # device memory the call used for the model's bytes: a ring of copy/hash groups, not a copy of the model
-               "device_staging_bytes": dict(getattr(sys.modules["paper_2510_00554_b200.model"], "LAST_HOST_STAGING", {}))}
+               "device_staging_bytes": dict(getattr(sys.modules["paper_2510_00554_b200.model"], "LAST_HOST_STAGING", {})),
+               "device_peak_extra_bytes": e2e_peak_extra}
         del model, host_entries
 
     # ---- the same call on ORDINARY (pageable) host memory -- numpy arrays, what a state dict loaded on the CPU or the
