@@ -239,7 +239,8 @@ STAGE_RING_GROUPS = 3                    # copy/hash groups the transfers may ru
 
 
 def _inplace_merkle_host(cfg: HashConfig, model: TensorMap, workers: int = 1) -> ModelDigestResult:
-    """Host tensors (page-locked or pageable, CUDA tensors mixed in) hashed while they arrive, in BOUNDED device memory.
+    """Host tensors (page-locked or pageable, CUDA tensors mixed in) hashed while they arrive, in BOUNDED device memory
+    (both constructions: Merkle leaves + tree, or LATTICE block sums).
 
     Every host tensor is cut into pieces of at most 64 MB at block boundaries -- the leaf sequence of the pieces
     is the leaf sequence of the tensor -- and the pieces are laid out in a RING of device memory that holds a few
@@ -391,7 +392,9 @@ def _inplace_merkle_host(cfg: HashConfig, model: TensorMap, workers: int = 1) ->
             for g in range(ahead):                         # page-locked sources: the link is busy from here on
                 issue(g)
         plan = _dev.ModelPlan.from_spans(keep, ptrs, sizes, bs, count=n)
-        hasher = _dev.MerkleModelHasher(plan, cfg.alg.value)
+        merkle = cfg.construction is Construction.MERKLE
+        hasher = _dev.MerkleModelHasher(plan, cfg.alg.value) if merkle else None
+        acc = None if merkle else _dev.LatticeAccumulator(1)     # LATTICE: leaves tagged LE64(k), summed (model.py:312-315)
         if n_pageable:
             for g in range(ahead):
                 issue(g)
@@ -399,16 +402,22 @@ def _inplace_merkle_host(cfg: HashConfig, model: TensorMap, workers: int = 1) ->
         for g, (_, _, leaf_end) in enumerate(groups):
             main.wait_event(copied[g])
             if leaf_end > begin:
-                hasher.run_leaves_only(begin, leaf_end)
+                if merkle:
+                    hasher.run_leaves_only(begin, leaf_end)
+                else:
+                    acc.add_model_leaves(plan, begin, leaf_end)
             begin = leaf_end
             done = torch.cuda.Event()
             done.record(main)
             hashed[g] = done
             if g + ahead < len(groups):
                 issue(g + ahead)
+        n_leaves = plan.leaf_count
+        if not merkle:
+            out, _, _ = acc.digests()                       # synchronises
+            return ModelDigestResult(LatticeDigest(out), cfg, n_leaves, aux_digest_bytes=acc.acc.numel() * 8)
         hasher.run_tree_only()
         root = Digest(cfg.alg, hasher.out_bytes())          # synchronises: all copies and kernels done
-        n_leaves = plan.leaf_count
         aux = hasher.leaves.numel() + hasher.work_bytes + (hasher.out.numel() if n_leaves > 1 else 0)
         return ModelDigestResult(root, cfg, n_leaves, aux_digest_bytes=aux)
     finally:
@@ -543,7 +552,7 @@ def inplace_hash(cfg: HashConfig, model: TensorMap, workers: int = 1) -> ModelDi
     if not all_resident:
         _require_nonempty(model)
         host_bytes = sum(buffer_nbytes(buf) for buf in buffers if not _is_cuda(buf))
-        if cfg.construction is Construction.MERKLE and host_bytes >= STAGE_PIPELINE_MIN_BYTES:
+        if host_bytes >= STAGE_PIPELINE_MIN_BYTES:
             return _inplace_merkle_host(cfg, model, workers)
     # an empty model is rejected by snt_model_plan_create (InvalidInput, model.py:166-168)
     plan = _dev.ModelPlan.from_spans(*_dev.device_spans(buffers), cfg.block_size)

@@ -256,6 +256,8 @@ def test_page_locked_model_copy_first_with_small_tensors_through_the_gather(pkg,
             assert res.block_count == tl.leaf_count(8192)
     assert len(taken) == 2 * len(ALGS)
     assert mm.LAST_HOST_STAGING["ring_bytes"] < mm.LAST_HOST_STAGING["host_bytes"]      # bounded device memory
+    lat = pkg.HashConfig(pkg.Construction.LATTICE, pkg.Strategy.IN_PLACE, pkg.CompressionAlg.BLAKE2B, 8192)
+    assert pkg.hash_model(lat, pkg.TensorMap(entries)).model_digest.data == corc.inplace_lattice(tl, 8192, 4)
     # block sizes on both sides of the piece size (a piece is a whole number of blocks, at least one)
     for bs in (64, 4 << 20):
         cfg = pkg.HashConfig(pkg.Construction.MERKLE, pkg.Strategy.IN_PLACE, _alg(pkg, "sha256"), bs)
@@ -291,6 +293,8 @@ def test_pageable_inputs_through_the_staging_ring(pkg, corc, monkeypatch, slot_k
         for workers in (1, 3):
             res = pkg.hash_model(cfg, pkg.TensorMap(entries), workers=workers)
             assert res.model_digest.data == corc.inplace_merkle(name, tl, 8192, 4), (name, workers)
+    lat = pkg.HashConfig(pkg.Construction.LATTICE, pkg.Strategy.IN_PLACE, pkg.CompressionAlg.BLAKE2B, 8192)
+    assert pkg.hash_model(lat, pkg.TensorMap(entries)).model_digest.data == corc.inplace_lattice(tl, 8192, 4)
     # the generic helper behind as_device_bytes (dataset shards, lattice / per-layer / coalesced model paths)
     monkeypatch.setattr(dv, "STAGE_DIRECT_MAX_BYTES", 1 << 20)
     big = rng.integers(0, 256, size=(7 << 20) + 321, dtype=np.uint8)
