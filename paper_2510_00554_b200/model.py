@@ -274,14 +274,15 @@ def _inplace_merkle_host(cfg: HashConfig, model: TensorMap, workers: int = 1) ->
     keep: List[object] = []
     n_pageable = 0
     for _, buf in entries:
-        nbytes = buffer_nbytes(buf)
+        is_tensor = isinstance(buf, torch.Tensor)
+        nbytes = buf.nbytes if is_tensor else buffer_nbytes(buf)
         if nbytes == 0:
             spans.append((CUDA, None, 0, 0))
-        elif _is_cuda(buf):
+        elif is_tensor and buf.is_cuda:
             t = _dev.as_device_bytes(buf, dev)
             keep.append(t)
             spans.append((CUDA, t, 0, nbytes))
-        elif isinstance(buf, torch.Tensor) and buf.is_pinned() and buf.is_contiguous():
+        elif is_tensor and buf.is_pinned() and buf.is_contiguous():
             if nbytes < small_limit:
                 spans.append((SMALL, buf, 0, nbytes))
             else:
@@ -310,6 +311,7 @@ def _inplace_merkle_host(cfg: HashConfig, model: TensorMap, workers: int = 1) ->
     offs = [0] * n                                         # ring offset of a PINNED / PAGEABLE span
     groups: List[Tuple[int, int, int]] = []               # (first span, end span, first leaf after the group)
     pos, small_pos, leaf, g_begin, g_bytes = 0, 0, 0, 0, 0
+    left = ring_need                                       # host bytes not yet assigned to a group
     small_src: List[int] = []
     small_len: List[int] = []
     small_off: List[int] = []
@@ -329,8 +331,11 @@ def _inplace_merkle_host(cfg: HashConfig, model: TensorMap, workers: int = 1) ->
             ptrs[i] = ring_base + pos
             pos += aligned(nbytes)
             g_bytes += aligned(nbytes)                     # the group's footprint in the ring, padding included
+            left -= aligned(nbytes)
         leaf += -(-nbytes // bs)
-        if g_bytes >= STAGE_CHUNK_BYTES or i == n - 1:
+        # groups shrink towards the end (half of what is left, at least 1/16 of a full group): the hashing of the
+        # LAST group is the only one no transfer hides
+        if g_bytes >= min(STAGE_CHUNK_BYTES, max(STAGE_CHUNK_BYTES >> 4, left >> 1)) or i == n - 1:
             groups.append((g_begin, i + 1, leaf))
             g_begin, g_bytes = i + 1, 0
 
@@ -342,9 +347,6 @@ def _inplace_merkle_host(cfg: HashConfig, model: TensorMap, workers: int = 1) ->
     side.wait_stream(main)
     ring.record_stream(side)
     side_handle = ctypes.c_void_p(side.cuda_stream)
-    if small_src:                                          # on the main stream, ahead of every leaf launch
-        _dev.gather_spans(np.array(small_src, dtype=np.uint64), np.array(small_len, dtype=np.uint64),
-                          np.array(small_off, dtype=np.uint64), 0, small_arena)
     staging = _dev.StagingRing.get(_dev.staging_threads(workers)) if n_pageable else None
     if staging is not None:
         staging.lock.acquire()                             # one staged hash at a time owns the pinned staging ring
@@ -391,6 +393,9 @@ def _inplace_merkle_host(cfg: HashConfig, model: TensorMap, workers: int = 1) ->
         if n_pageable == 0:
             for g in range(ahead):                         # page-locked sources: the link is busy from here on
                 issue(g)
+        if small_src:                                      # on the main stream, ahead of every leaf launch
+            _dev.gather_spans(np.array(small_src, dtype=np.uint64), np.array(small_len, dtype=np.uint64),
+                              np.array(small_off, dtype=np.uint64), 0, small_arena)
         plan = _dev.ModelPlan.from_spans(keep, ptrs, sizes, bs, count=n)
         merkle = cfg.construction is Construction.MERKLE
         hasher = _dev.MerkleModelHasher(plan, cfg.alg.value) if merkle else None
