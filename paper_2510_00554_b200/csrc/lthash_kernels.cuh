@@ -25,7 +25,10 @@ namespace snt {
 // better on ragged samples (2 M: 2.94 -> 2.06 ms), worse on samples of one length (CIFAR 194 -> 220 us) -- and ragged
 // samples take the lane kernel anyway, so the grid keeps the unrolled rounds.
 constexpr bool LT_GRID_ROLLED = SNT_LT_GRID_ROLLED != 0;
-constexpr int LT_THREADS = 64;
+#ifndef SNT_LT_THREADS
+#define SNT_LT_THREADS 64
+#endif
+constexpr int LT_THREADS = SNT_LT_THREADS;
 constexpr int LT_LANES = 32;                 // u16 lanes per digest
 constexpr int LT_SMEM_SOURCES = 128;         // per-CTA shared accumulators: 128 x 32 x 4 B = 16 KiB
 
