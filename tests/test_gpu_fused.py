@@ -255,6 +255,23 @@ def test_lthash_lanes_kernel_block_boundaries_and_alignments(dev, corc):
             assert dig.cpu().numpy().tobytes() == want_dig, (n, align, uniform)
 
 
+def test_resident_model_tiny_trees_root_lands_in_pinned_host_memory(porc):
+    """One- and two-leaf device-resident models through the cached path, whose output buffer is page-locked HOST memory
+    (the last kernel -- or, for a single leaf, an asynchronous device-to-host copy of the leaf digest -- writes the root
+    there): repeated calls, every algorithm."""
+    import paper_2510_00554_b200 as pkg
+
+    for alg in ("sha256", "blake2b", "sha3-256"):
+        cfg = pkg.HashConfig(pkg.Construction.MERKLE, pkg.Strategy.IN_PLACE, pkg.CompressionAlg.from_name(alg))
+        for size in (1, 100, 8192, 8193, 3 * 8192):
+            h = np.random.default_rng(size).integers(0, 256, size=size, dtype=np.uint8)
+            m = pkg.TensorMap([("a", torch.from_numpy(h).cuda())])
+            want = porc.inplace_merkle(alg, [h.tobytes()], 8192)
+            for _ in range(3):
+                assert pkg.hash_model(cfg, m).model_digest.data == want, (alg, size)
+            assert m.__dict__["_resident"].hasher.out.device.type == "cpu"
+
+
 def test_resident_model_cache_revalidates_every_call(porc):
     """hash_model on a TensorMap of CUDA tensors re-uses plan and workspace, launches before it re-checks the tensors,
     and still never returns a digest for bytes it did not check: content changes, re-pointed tensors, resized tensors
