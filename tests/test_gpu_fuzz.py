@@ -1,0 +1,161 @@
+"""Randomised parity: models and datasets drawn at random (sizes, alignments, where the bytes live, block size,
+algorithm, construction, schedule), hashed through the public API and compared with the C oracle. Every case is a
+function of its seed, printed on failure. The default budget is a few seconds; SNT_FUZZ_SECONDS=600 makes it a soak.
+"""
+
+import os
+import time
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+ALGS = ("sha256", "blake2b", "sha3-256")
+BUDGET = float(os.environ.get("SNT_FUZZ_SECONDS", "12"))
+
+
+@pytest.fixture(scope="module")
+def pkg():
+    import paper_2510_00554_b200 as pkg
+    from paper_2510_00554_b200 import _native
+
+    assert torch.cuda.is_available(), "gpu tests need a CUDA device"
+    _native.load()
+    return pkg
+
+
+def _random_sizes(rng, n, big):
+    kinds = rng.integers(0, 6, size=n)
+    out = []
+    for k in kinds:
+        if k == 0:
+            out.append(0)
+        elif k == 1:
+            out.append(int(rng.integers(1, 300)))
+        elif k == 2:
+            out.append(int(rng.integers(1, 40)) * 8192)                       # whole blocks
+        elif k == 3:
+            out.append(int(rng.integers(1, 40)) * 8192 + int(rng.integers(1, 8192)))
+        elif k == 4:
+            out.append(int(rng.integers(60_000, 70_000)))                     # around the small-tensor threshold
+        else:
+            out.append(int(rng.integers(1, big)))
+    return out
+
+
+def test_random_models_against_the_c_oracle(pkg, corc, monkeypatch):
+    from paper_2510_00554_b200 import _native, device as dv, model as mm
+
+    lib = _native.load()
+    deadline = time.monotonic() + BUDGET
+    seed0 = int(os.environ.get("SNT_FUZZ_SEED", "1000"))
+    case = 0
+    try:
+        while time.monotonic() < deadline or case < 3:
+            seed = seed0 + case
+            case += 1
+            rng = np.random.default_rng(seed)
+            n = int(rng.integers(1, 24))
+            host_mode = int(rng.integers(0, 4))            # 0 all CUDA, 1 all pinned, 2 pageable mix, 3 everything mixed
+            big = int(rng.choice([20_000, 3 << 20, 12 << 20])) if host_mode else int(rng.choice([20_000, 1 << 20]))
+            sizes = _random_sizes(rng, n, big)
+            if sum(sizes) == 0:
+                sizes[0] = 77
+            arena = rng.integers(0, 256, size=sum(sizes) + 64 * n + 64, dtype=np.uint8)
+            host, entries, pos, base_cuda = [], [], 0, None
+            for i, s in enumerate(sizes):
+                pos += int(rng.integers(0, 17)) if rng.random() < 0.3 else 0     # odd addresses now and then
+                h = arena[pos:pos + s]
+                pos += s
+                host.append(h)
+                where = {0: 0, 1: 1, 2: int(rng.integers(2, 5)), 3: int(rng.integers(0, 5))}[host_mode]
+                if where == 0:
+                    if base_cuda is None:
+                        base_cuda = torch.from_numpy(arena).cuda()                          # views into ONE device buffer
+                    entries.append((f"t{i}", base_cuda[pos - s:pos]))
+                elif where == 1:
+                    entries.append((f"t{i}", torch.from_numpy(h.copy()).pin_memory()))
+                elif where == 2:
+                    entries.append((f"t{i}", h.tobytes()))
+                elif where == 3:
+                    entries.append((f"t{i}", h))                                           # numpy view, any alignment
+                else:
+                    entries.append((f"t{i}", torch.from_numpy(h.copy())))
+            bs = int(rng.choice([64, 1024, 8192, 8192, 1 << 16]))
+            alg = ALGS[int(rng.integers(0, 3))]
+            lattice = rng.random() < 0.25
+            schedule = int(rng.integers(0, 3))
+            # small staging parameters so that rings wrap and pieces split at test sizes
+            monkeypatch.setattr(mm, "STAGE_PIPELINE_MIN_BYTES", int(rng.choice([1 << 16, 32 << 20])))
+            monkeypatch.setattr(mm, "STAGE_CHUNK_BYTES", int(rng.choice([1 << 20, 3 << 20, 256 << 20])))
+            monkeypatch.setattr(mm, "STAGE_PIECE_BYTES", int(rng.choice([1 << 19, 1 << 20, 64 << 20])))
+            monkeypatch.setattr(dv, "STAGE_SLOT_BYTES", int(rng.choice([1 << 20, 32 << 20])))
+            monkeypatch.setattr(dv, "STAGE_PIECE_BYTES", int(rng.choice([1 << 18, 4 << 20])))
+            lib.snt_merkle_schedule(schedule)
+            tl = corc.TensorList(host)
+            what = (seed, sizes, host_mode, bs, alg, lattice, schedule)
+            model = pkg.TensorMap(entries)
+            if lattice:
+                cfg = pkg.HashConfig(pkg.Construction.LATTICE, pkg.Strategy.IN_PLACE, pkg.CompressionAlg.BLAKE2B, bs)
+                want = corc.inplace_lattice(tl, bs, 4)
+            else:
+                cfg = pkg.HashConfig(pkg.Construction.MERKLE, pkg.Strategy.IN_PLACE, pkg.CompressionAlg.from_name(alg), bs)
+                want = corc.inplace_merkle(alg, tl, bs, 4)
+            for _ in range(2):                                                              # the second call may hit the cache
+                res = pkg.hash_model(cfg, model)
+                assert res.model_digest.data == want, what
+                assert res.block_count == tl.leaf_count(bs), what
+    finally:
+        lib.snt_merkle_schedule(_native.SCHEDULE_PERSISTENT)
+    print(f"{case} random models")
+
+
+def test_random_datasets_against_the_c_oracle(pkg, corc):
+    from paper_2510_00554_b200 import _native, dataset as dsm, device as dev
+
+    lib = _native.load()
+    deadline = time.monotonic() + BUDGET
+    seed0 = int(os.environ.get("SNT_FUZZ_SEED", "5000"))
+    case = 0
+    try:
+        while time.monotonic() < deadline or case < 3:
+            seed = seed0 + case
+            case += 1
+            rng = np.random.default_rng(seed)
+            n = int(rng.choice([1, 7, 33, 500, 5000, 40_000]))
+            shape = int(rng.integers(0, 4))
+            if shape == 0:
+                lens = np.full(n, int(rng.choice([0, 8, 120, 128, 3072])), dtype=np.uint64)        # one length
+            elif shape == 1:
+                lens = (rng.integers(4, 260, size=n) * 4).astype(np.uint64)                          # token arrays
+            elif shape == 2:
+                lens = rng.integers(0, 700, size=n).astype(np.uint64)
+            else:
+                lens = rng.choice(np.array([0, 1, 119, 120, 121, 127, 128, 129, 248, 256, 9000], dtype=np.uint64), size=n)
+            gap = int(rng.choice([0, 0, 1, 3, 4, 8]))
+            offs = np.zeros(n, dtype=np.uint64)
+            if n > 1:
+                np.cumsum(lens[:-1] + np.uint64(gap), out=offs[1:])
+            shard = rng.integers(0, 256, size=int(offs[-1] + lens[-1]) + 16, dtype=np.uint8)
+            n_src = int(rng.choice([1, 3, 16, 129, 300]))
+            src = rng.integers(0, n_src, size=n)
+            ids = rng.integers(0, 2**63, size=n).astype(np.uint64)
+            schedule = int(rng.integers(0, 3))
+            lib.snt_merkle_schedule(schedule)
+            what = (seed, n, shape, gap, n_src, schedule)
+            want_sums, want_counts = corc.lthash_samples(shard, offs, lens, ids, src.astype(np.uint32), n_src, 4)
+            ds = dsm.DeviceDataset.from_host(shard, offs, lens, ids, src, list(range(n_src)))
+            if rng.random() < 0.3:
+                ds.uniform = None                                                                    # "not known": lanes
+            acc = dev.LatticeAccumulator(n_src)
+            a = int(rng.integers(0, n))
+            ds.accumulate(acc, 0, a)                                                                 # two launches: ranges add up
+            ds.accumulate(acc, a, n)
+            out, counts, status = acc.digests()
+            assert (status, counts) == (0, list(want_counts)), what
+            assert out == want_sums, what
+    finally:
+        lib.snt_merkle_schedule(_native.SCHEDULE_PERSISTENT)
+    print(f"{case} random datasets")
