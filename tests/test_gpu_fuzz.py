@@ -159,3 +159,38 @@ def test_random_datasets_against_the_c_oracle(pkg, corc):
     finally:
         lib.snt_merkle_schedule(_native.SCHEDULE_PERSISTENT)
     print(f"{case} random datasets")
+
+
+def test_random_models_per_layer_and_coalesced_against_the_python_oracle(pkg, porc):
+    """The strategies that move data before hashing: per-layer digests + model digest and the
+    coalesced digest, both constructions, on small random models whose tensors live on the GPU or on the host."""
+    deadline = time.monotonic() + BUDGET
+    seed0 = int(os.environ.get("SNT_FUZZ_SEED", "9000"))
+    case = 0
+    while time.monotonic() < deadline or case < 3:
+        seed = seed0 + case
+        case += 1
+        rng = np.random.default_rng(seed)
+        n = int(rng.integers(1, 12))
+        bs = int(rng.choice([64, 256, 1024]))
+        sizes = [int(rng.choice([0, 1, bs - 1, bs, bs + 1, 3 * bs, int(rng.integers(1, 20 * bs))])) for _ in range(n)]
+        if sum(sizes) == 0:
+            sizes[0] = 5
+        host = [rng.integers(0, 256, size=s, dtype=np.uint8).tobytes() for s in sizes]
+        on_gpu = rng.random() < 0.5
+        entries = [(f"l{i}", torch.frombuffer(bytearray(h), dtype=torch.uint8).cuda() if (on_gpu and h) else h)
+                   for i, h in enumerate(host)]
+        model = pkg.TensorMap(entries)
+        alg = ALGS[int(rng.integers(0, 3))]
+        what = (seed, sizes, bs, alg, on_gpu)
+        m_cfg = lambda strat: pkg.HashConfig(pkg.Construction.MERKLE, strat, pkg.CompressionAlg.from_name(alg), bs)   # noqa: E731
+        l_cfg = lambda strat: pkg.HashConfig(pkg.Construction.LATTICE, strat, pkg.CompressionAlg.BLAKE2B, bs)          # noqa: E731
+        root, layers = porc.per_layer_merkle(alg, host, bs)
+        res = pkg.hash_model(m_cfg(pkg.Strategy.PER_LAYER), model)
+        assert res.model_digest.data == root and [d.data for d in res.layer_digests.values()] == layers, what
+        root, layers = porc.per_layer_lattice(host, bs)
+        res = pkg.hash_model(l_cfg(pkg.Strategy.PER_LAYER), model)
+        assert res.model_digest.data == root and [d.data for d in res.layer_digests.values()] == layers, what
+        assert pkg.hash_model(m_cfg(pkg.Strategy.COALESCED), model).model_digest.data == porc.coalesced_merkle(alg, host, bs), what
+        assert pkg.hash_model(l_cfg(pkg.Strategy.COALESCED), model).model_digest.data == porc.coalesced_lattice(host, bs), what
+    print(f"{case} random models x 4 strategy/construction pairs")
