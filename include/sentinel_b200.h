@@ -174,6 +174,15 @@ int snt_lthash_samples_shaped(const void* d_shard, const uint64_t* d_off, const 
                               uint32_t n_sources, uint64_t* d_acc, uint64_t* d_counts, void* d_digests,
                               uint64_t* d_status, uint32_t shape, snt_stream_t stream);
 
+/* The loader-side form of process_batch (dataset.py:74-86; the on-the-fly use of the paper): a batch as a GPU data
+ * loader holds it -- n rows of row_bytes bytes each in one device tensor -- with the raw source id of every row.
+ * The slot of a row is found inside the kernel by binary search of d_src_ids[i] in d_table, the n_sources declared
+ * source ids in ascending order; an id that is not in the table is skipped and counted in *d_status. One launch
+ * per batch, nothing else. */
+int snt_lthash_rows(const void* d_rows, uint64_t row_bytes, uint64_t n, const uint64_t* d_ids,
+                    const int64_t* d_src_ids, const int64_t* d_table, uint32_t n_sources, uint64_t* d_acc,
+                    uint64_t* d_counts, void* d_digests, uint64_t* d_status, snt_stream_t stream);
+
 /* inplace_hash, LATTICE construction (model.py:312-315): leaves
  * [leaf_begin, leaf_end) tagged LE64(k), summed into d_acc[32] / d_counts[1]. */
 int snt_lthash_model(const snt_model_plan* plan, uint64_t leaf_begin, uint64_t leaf_end,

@@ -56,6 +56,8 @@ SIGNATURES = {
     "snt_device_reads_pinned_host": (c_int, []),
     "snt_lthash_samples_shaped": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_uint64, c_uint32,
                                           c_void_p, c_void_p, c_void_p, c_void_p, c_uint32, c_void_p]),
+    "snt_lthash_rows": (c_int, [c_void_p, c_uint64, c_uint64, c_void_p, c_void_p, c_void_p, c_uint32,
+                                c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "snt_lthash_model": (c_int, [c_void_p, c_uint64, c_uint64, c_void_p, c_void_p, c_void_p, c_void_p]),
     "snt_lthash_model_layers": (c_int, [c_void_p, c_uint64, c_uint64, c_void_p, c_void_p, c_void_p, c_void_p]),
     "snt_merkle_roots_segmented": (c_int, [c_int, c_void_p, POINTER(c_uint64), c_uint32, c_void_p, c_void_p,

@@ -15,6 +15,7 @@
 #include "gather_kernels.cuh"
 #include "lthash_kernels.cuh"
 #include "lthash_lanes.cuh"
+#include "lthash_quad.cuh"
 #include "merkle_fused.cuh"
 #include "merkle_kernels.cuh"
 
@@ -480,6 +481,54 @@ int launch_blocks(const uint8_t* base, const uint64_t* off, const uint64_t* len,
     return SNT_OK;
 }
 
+// Largest launch that takes the four-lanes-per-item kernel (SNT_LT_QUAD_MAX overrides it for the probes).
+uint64_t quad_max_items() {
+    static const uint64_t v = [] {
+        const char* e = getenv("SNT_LT_QUAD_MAX");
+        return e ? static_cast<uint64_t>(strtoull(e, nullptr, 10)) : LT_QUAD_MAX_ITEMS;
+    }();
+    return v;
+}
+
+// Four lanes per item (lthash_quad.cuh): small launches, where latency is everything.
+template <class Items>
+int launch_lthash_quad(const Items& items, uint64_t n, uint32_t n_sources, unsigned long long* acc,
+                       unsigned long long* counts, uint8_t* dig, unsigned long long* status, cudaStream_t s) {
+    if (n == 0) return SNT_OK;
+    constexpr int quads = LT_QUAD_THREADS / 4;
+    const unsigned grid = static_cast<unsigned>((n + quads - 1) / quads);
+    const size_t regions = static_cast<size_t>(quads) * QUAD_REGION_BYTES;
+    if (n_sources <= static_cast<uint32_t>(LT_SMEM_SOURCES)) {
+        const size_t smem = regions + static_cast<size_t>(n_sources) * (LT_LANES + 1) * sizeof(uint32_t);
+        lthash_quad_kernel<Items, true><<<grid, LT_QUAD_THREADS, smem, s>>>(items, n, n_sources, acc, counts, dig, status);
+    } else {
+        lthash_quad_kernel<Items, false><<<grid, LT_QUAD_THREADS, regions, s>>>(items, n, n_sources, acc, counts, dig, status);
+    }
+    SNT_CUDA(cudaGetLastError());
+    ++g_launches;
+    return SNT_OK;
+}
+
+// One thread per item on a plain grid (lthash_kernel).
+template <class Items>
+int launch_lthash_grid(const Items& items, uint64_t n, uint32_t n_sources, unsigned long long* acc,
+                       unsigned long long* counts, uint8_t* dig, unsigned long long* status, cudaStream_t s) {
+    if (n == 0) return SNT_OK;
+    const uint64_t grid = (n + LT_THREADS - 1) / LT_THREADS;
+    if (grid > 0x7fffffffull) return SNT_ERR_INVALID_INPUT;
+    if (n_sources <= static_cast<uint32_t>(LT_SMEM_SOURCES)) {
+        const size_t smem = LT_STAGE_BYTES + static_cast<size_t>(n_sources) * (LT_LANES + 1) * sizeof(uint32_t);
+        lthash_kernel<Items, true><<<static_cast<unsigned>(grid), LT_THREADS, smem, s>>>(
+            items, n, n_sources, acc, counts, dig, status);
+    } else {
+        lthash_kernel<Items, false><<<static_cast<unsigned>(grid), LT_THREADS, LT_STAGE_BYTES, s>>>(
+            items, n, n_sources, acc, counts, dig, status);
+    }
+    SNT_CUDA(cudaGetLastError());
+    ++g_launches;
+    return SNT_OK;
+}
+
 template <class Items, bool SMEM_ACC>
 int launch_lthash_chains(const Items& items, uint64_t n, uint32_t n_sources, unsigned long long* acc,
                          unsigned long long* counts, uint8_t* dig, unsigned long long* status, cudaStream_t s) {
@@ -549,23 +598,13 @@ int launch_lthash(const Items& items, uint64_t n, uint32_t n_sources, uint64_t* 
     // Samples of unknown or ragged length take the persistent lanes (a lane fetches its next sample the moment it
     // finishes one: 2 M hellaswag-shaped samples 2.94 -> 1.09 ms unsorted, 40 k 93 -> 65 us); samples the caller
     // declares to be of ONE length keep the plain grid, which has less bookkeeping per block (CIFAR 194 vs 217 us).
+    if constexpr (!Items::LONG_ITEMS) if (schedule == SNT_SCHEDULE_PERSISTENT && n <= quad_max_items())
+        return launch_lthash_quad(items, n, n_sources, acc, counts, dig, status, s);     // a loader batch: latency, not throughput
     if constexpr (!Items::LONG_ITEMS) if (schedule == SNT_SCHEDULE_PERSISTENT && shape != SNT_SAMPLES_UNIFORM) {
         if (smem_acc) return launch_lthash_lanes<Items, true>(items, n, n_sources, acc, counts, dig, status, s);
         return launch_lthash_lanes<Items, false>(items, n, n_sources, acc, counts, dig, status, s);
     }
-    const uint64_t grid = (n + LT_THREADS - 1) / LT_THREADS;
-    if (grid > 0x7fffffffull) return SNT_ERR_INVALID_INPUT;
-    if (smem_acc) {
-        const size_t smem = LT_STAGE_BYTES + static_cast<size_t>(n_sources) * (LT_LANES + 1) * sizeof(uint32_t);
-        lthash_kernel<Items, true><<<static_cast<unsigned>(grid), LT_THREADS, smem, s>>>(
-            items, n, n_sources, acc, counts, dig, status);
-    } else {
-        lthash_kernel<Items, false><<<static_cast<unsigned>(grid), LT_THREADS, LT_STAGE_BYTES, s>>>(
-            items, n, n_sources, acc, counts, dig, status);
-    }
-    SNT_CUDA(cudaGetLastError());
-    ++g_launches;
-    return SNT_OK;
+    return launch_lthash_grid(items, n, n_sources, acc, counts, dig, status, s);
 }
 
 }  // namespace
@@ -681,6 +720,28 @@ int snt_lthash_samples_shaped(const void* d_shard, const uint64_t* d_off, const 
     items.slot = d_slot;
     return launch_lthash(items, n, n_sources, d_acc, d_counts, d_digests, d_status,
                          static_cast<cudaStream_t>(stream), shape);
+}
+
+int snt_lthash_rows(const void* d_rows, uint64_t row_bytes, uint64_t n, const uint64_t* d_ids,
+                    const int64_t* d_src_ids, const int64_t* d_table, uint32_t n_sources, uint64_t* d_acc,
+                    uint64_t* d_counts, void* d_digests, uint64_t* d_status, snt_stream_t stream) {
+    if (n_sources == 0 || !d_acc || !d_counts || !d_table) return SNT_ERR_INVALID_INPUT;
+    if (n && (!d_ids || !d_src_ids || (row_bytes && !d_rows))) return SNT_ERR_INVALID_INPUT;
+    RowItems items;
+    items.rows = static_cast<const uint8_t*>(d_rows);
+    items.row_bytes = row_bytes;
+    items.ids = d_ids;
+    items.src = reinterpret_cast<const long long*>(d_src_ids);
+    items.table = reinterpret_cast<const long long*>(d_table);
+    items.n_table = n_sources;
+    auto* acc = reinterpret_cast<unsigned long long*>(d_acc);
+    auto* counts = reinterpret_cast<unsigned long long*>(d_counts);
+    auto* status = reinterpret_cast<unsigned long long*>(d_status);
+    auto* dig = static_cast<uint8_t*>(d_digests);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (n <= quad_max_items() && g_schedule.load() == SNT_SCHEDULE_PERSISTENT)
+        return launch_lthash_quad(items, n, n_sources, acc, counts, dig, status, s);
+    return launch_lthash_grid(items, n, n_sources, acc, counts, dig, status, s);
 }
 
 int snt_lthash_model(const snt_model_plan* plan, uint64_t leaf_begin, uint64_t leaf_end, uint64_t* d_acc,

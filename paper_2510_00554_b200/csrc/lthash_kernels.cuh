@@ -61,6 +61,36 @@ struct SampleItems {
     }
 };
 
+// Loader batches (dataset.StreamingDatasetHasher): n fixed-size rows of ONE tensor, as a GPU data loader holds a
+// batch. The source slot of a row is found INSIDE the kernel, by binary search of its source id in the sorted
+// table of declared ids (an id that is not there gets slot n_table = undeclared, counted in the status word,
+// dataset.py:78-80) -- one launch per batch and no index arithmetic around it.
+struct RowItems {
+    const uint8_t* __restrict__ rows;
+    uint64_t row_bytes;
+    const uint64_t* __restrict__ ids;
+    const long long* __restrict__ src;
+    const long long* __restrict__ table;
+    uint32_t n_table;
+    static constexpr int TAG_WORDS = 1;
+    static constexpr bool LONG_ITEMS = false;
+    SNT_HD LtItem get(uint64_t i) const {
+        LtItem it;
+        it.ptr = rows + i * row_bytes;
+        it.len = row_bytes;
+        it.tag = ids[i];
+        it.tag1 = 0;
+        const long long want = src[i];
+        uint32_t lo = 0, hi = n_table;                 // first entry >= want
+        while (lo < hi) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (table[mid] < want) lo = mid + 1; else hi = mid;
+        }
+        it.slot = (lo < n_table && table[lo] == want) ? lo : n_table;
+        return it;
+    }
+};
+
 // Model blocks hashed in place: item i is leaf k = leaf_begin + i of the block
 // table, tagged with the global block counter k (model.py:312).
 struct LeafItems {

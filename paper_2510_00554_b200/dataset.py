@@ -438,9 +438,9 @@ class StreamingDatasetHasher:
     The reference's loader-side protocol is ``process_batch(batch, acc)`` over host records
     (dataset.py:74-86, the on-the-fly use of PAPER.md:504-515). Here a batch is what a GPU data
     loader already holds: a ``[B, ...]`` tensor of fixed-size samples (any dtype, CUDA or pinned
-    host memory) plus ``sample_ids`` and ``source_ids`` tensors. ``update`` maps source ids to
-    accumulator slots on the device, enqueues one ``snt_lthash_samples`` launch on the current
-    stream and returns at once; nothing is synchronised until ``finalize``. The result equals
+    host memory) plus ``sample_ids`` and ``source_ids`` tensors. ``update`` enqueues ONE launch on the
+    current stream (``snt_lthash_rows``: the kernel maps source ids to accumulator slots itself) and
+    returns at once; nothing is synchronised until ``finalize``. The result equals
     ``digest_dataset`` over the same samples for any batch size and order.
     """
 
@@ -451,33 +451,29 @@ class StreamingDatasetHasher:
             raise ValidationError("at least one declared source is required")
         self._table = torch.tensor(self.source_ids, dtype=torch.int64, device=self._dev)
         self._acc = _dev.LatticeAccumulator(len(self.source_ids))
-        self._rows: Dict[Tuple[int, int], Tuple[torch.Tensor, torch.Tensor]] = {}   # (B, row bytes) -> offsets, lengths
 
-    def _row_index(self, n: int, row_bytes: int) -> Tuple[torch.Tensor, torch.Tensor]:
-        key = (n, row_bytes)
-        if key not in self._rows:
-            off = torch.arange(n, dtype=torch.int64, device=self._dev) * row_bytes
-            self._rows[key] = (off, torch.full((n,), row_bytes, dtype=torch.int64, device=self._dev))
-        return self._rows[key]
+    def _int64_on_device(self, values, n: int, what: str) -> torch.Tensor:
+        t = values if isinstance(values, torch.Tensor) else torch.as_tensor(values)
+        if t.device != self._dev or t.dtype != torch.int64 or not t.is_contiguous():
+            t = t.to(self._dev, dtype=torch.int64, non_blocking=True).contiguous()
+        t = t.reshape(-1)
+        if t.numel() != n:
+            raise ValidationError(f"{what} needs one entry per row of the batch")
+        return t
 
     def update(self, data: torch.Tensor, sample_ids, source_ids) -> None:
-        """Fold one batch in: row i of ``data`` is sample ``sample_ids[i]`` of source ``source_ids[i]``."""
+        """Fold one batch in: row i of ``data`` is sample ``sample_ids[i]`` of source ``source_ids[i]``.
+
+        ONE launch (``snt_lthash_rows``): the kernel derives row addresses from the row size and looks the source id
+        of every row up in the table of declared ids itself; an undeclared id is flagged in the status word and
+        raises in ``finalize``."""
         if data.dim() < 1 or data.shape[0] == 0:
             return
         n = int(data.shape[0])
         flat = _dev.as_device_bytes(data, self._dev)
-        row_bytes = flat.numel() // n
-        off, ln = self._row_index(n, row_bytes)
-        ids = torch.as_tensor(sample_ids).to(self._dev, dtype=torch.int64, non_blocking=True).reshape(-1)
-        src = torch.as_tensor(source_ids).to(self._dev, dtype=torch.int64, non_blocking=True).reshape(-1)
-        if ids.numel() != n or src.numel() != n:
-            raise ValidationError("sample_ids and source_ids need one entry per row of the batch")
-        pos = torch.searchsorted(self._table, src).clamp_(max=len(self.source_ids) - 1)
-        # an undeclared source gets slot n_sources: the kernel flags it in the status word (checked in finalize)
-        slots = torch.where(self._table[pos] == src, pos, torch.full_like(pos, len(self.source_ids))).to(torch.int32)
-        if flat.numel() == 0:
-            flat = torch.zeros(16, dtype=torch.uint8, device=self._dev)
-        self._acc.add_samples(flat, off, ln, ids, slots, uniform=True)      # rows of one tensor: one length
+        ids = self._int64_on_device(sample_ids, n, "sample_ids")
+        src = self._int64_on_device(source_ids, n, "source_ids")
+        self._acc.add_rows(flat, flat.numel() // n, n, ids, src, self._table)
 
     def finalize(self) -> Dict[int, Tuple[LatticeDigest, int]]:
         """Per-source digests and counts, ordered by source id; raises if any batch named an undeclared source."""

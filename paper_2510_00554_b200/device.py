@@ -603,6 +603,15 @@ class LatticeAccumulator:
                                            _ptr(self.status), shape, _stream())
         _native.check(rc, "snt_lthash_samples_shaped")
 
+    def add_rows(self, rows: torch.Tensor, row_bytes: int, n: int, ids: torch.Tensor, source_ids: torch.Tensor,
+                 table: torch.Tensor, digests: Optional[torch.Tensor] = None) -> None:
+        """``snt_lthash_rows``: n rows of ``row_bytes`` bytes in one flat device tensor, raw source ids (int64) looked up
+        in ``table`` (the declared ids, sorted, int64, on the device) inside the kernel. One launch."""
+        lib = _native.load()
+        rc = lib.snt_lthash_rows(_ptr(rows), row_bytes, n, _ptr(ids), _ptr(source_ids), _ptr(table), self.n_sources,
+                                 _ptr(self.acc), _ptr(self.counts), _ptr(digests), _ptr(self.status), _stream())
+        _native.check(rc, "snt_lthash_rows")
+
     def add_model_leaves(self, plan: ModelPlan, leaf_begin: int, leaf_end: int,
                          digests: Optional[torch.Tensor] = None) -> None:
         lib = _native.load()
