@@ -4,7 +4,7 @@
 
 All three Merkle schedules (persistent chains + reducer, fused single launch, grid) on ragged / unaligned models
 whose SMs get more chains than worker warps (so the parked-state FIFO runs), shard ranges with forced levels, and
-the LtHash kernels (grid, forced chains, persistent lanes). SANITIZE_ONLY=lthash skips the Merkle part. Results are checked against hashlib, so a silent corruption fails too.
+the LtHash kernels (grid, forced chains, persistent lanes, four lanes per item). SANITIZE_ONLY=lthash skips the Merkle part. Results are checked against hashlib, so a silent corruption fails too.
 """
 import hashlib
 import os
@@ -87,4 +87,10 @@ for schedule in (_native.SCHEDULE_FUSED, _native.SCHEDULE_GRID, _native.SCHEDULE
     out, counts, status = acc.digests()
     assert out == want and status == 0 and sum(counts) == n, schedule
 lib.snt_merkle_schedule(_native.SCHEDULE_PERSISTENT)
+# a small launch: the four-lanes-per-item kernel (the first 1,000 samples in two calls, then the rest through the lanes)
+acc = dev.LatticeAccumulator(n_src)
+for a, b in ((0, 700), (700, 1000), (1000, n)):
+    acc.add_samples(d_args[0], *(t[a:b] for t in d_args[1:]))
+out, counts, status = acc.digests()
+assert out == want and status == 0 and sum(counts) == n, "quad + lanes"
 print("sanitize smoke ok")
