@@ -775,56 +775,94 @@ int snt_merkle_roots_segmented(int alg, const void* d_digests, const uint64_t* s
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const uint8_t* in = static_cast<const uint8_t*>(d_digests);
     uint8_t* out = static_cast<uint8_t*>(d_out);
-    // segments that fit one CTA (<= 2^max_levels digests) share ONE launch; the rest go one by one
-    const uint64_t cta_cap = 1ull << max_levels(alg);
-    std::vector<uint64_t> table;           // [begin, count] per small segment, then the u32 output indices
-    std::vector<uint32_t> out_idx;
+    // Segments that fit one CTA (<= 2^max_levels digests) are finished by ONE launch, one CTA each. Larger ones (up
+    // to 2^(2 * max_levels) digests, as far as the workspace goes) first lose their bottom max_levels levels in ONE
+    // launch over all their groups (merkle_reduce_groups_kernel, nodes into the workspace) and then join that same
+    // launch. Anything larger goes through the ordinary reducer chain, one tree after the other.
+    const uint32_t cap = max_levels(alg);
+    const uint64_t cta_cap = 1ull << cap;
+    const uint64_t work_nodes = d_work ? work_bytes / dlen : 0;
+    std::vector<uint64_t> seg_rows;        // [address, count] per segment of the final launch
+    std::vector<uint32_t> seg_out;
+    std::vector<uint64_t> grp_rows;        // [address, count, group] per group of the first launch
+    std::vector<uint32_t> grp_out;
+    std::vector<uint32_t> chained;         // segments left to the reducer chain
+    uint64_t inter = 0;                    // workspace nodes handed out so far
+    const uint64_t in_addr = reinterpret_cast<uint64_t>(in), work_addr = reinterpret_cast<uint64_t>(d_work);
     for (uint32_t t = 0; t < n_segments; ++t) {
         if (seg_first[t + 1] < seg_first[t]) return SNT_ERR_INVALID_INPUT;
         const uint64_t count = seg_first[t + 1] - seg_first[t];
         if (count == 0 && !d_empty_digest) return SNT_ERR_INVALID_INPUT;
+        const uint64_t addr = in_addr + seg_first[t] * dlen;
         if (count <= cta_cap) {
-            table.push_back(seg_first[t]);
-            table.push_back(count);
-            out_idx.push_back(t);
+            seg_rows.push_back(addr);
+            seg_rows.push_back(count);
+            seg_out.push_back(t);
+            continue;
         }
+        const uint64_t groups = (count + cta_cap - 1) >> cap;
+        if (groups > cta_cap || inter + groups > work_nodes || grp_out.size() + groups > 0x7fffffffull) {
+            chained.push_back(t);
+            continue;
+        }
+        for (uint64_t g = 0; g < groups; ++g) {
+            grp_rows.push_back(addr);
+            grp_rows.push_back(count);
+            grp_rows.push_back(g);
+            grp_out.push_back(static_cast<uint32_t>(inter + g));
+        }
+        seg_rows.push_back(work_addr + inter * dlen);
+        seg_rows.push_back(groups);
+        seg_out.push_back(t);
+        inter += groups;
     }
-    if (!out_idx.empty()) {
-        const size_t n_small = out_idx.size();
-        const size_t seg_bytes = table.size() * sizeof(uint64_t);
-        table.resize(table.size() + (n_small + 1) / 2);
-        memcpy(reinterpret_cast<uint8_t*>(table.data()) + seg_bytes, out_idx.data(), n_small * sizeof(uint32_t));
+    // the reducer chain uses the workspace too: those trees go first, before the group nodes are written into it
+    for (uint32_t t : chained) {
+        const int rc = snt_merkle_root(alg, in + seg_first[t] * dlen, seg_first[t + 1] - seg_first[t], d_work, work_bytes,
+                                       out + static_cast<size_t>(t) * dlen, stream);
+        if (rc != SNT_OK) return rc;
+    }
+    // both tables in one upload: [group rows | segment rows | group outputs | segment outputs]
+    const size_t n_grp = grp_out.size(), n_seg = seg_out.size();
+    if (n_seg) {
+        std::vector<uint64_t> table(grp_rows);
+        table.insert(table.end(), seg_rows.begin(), seg_rows.end());
+        const size_t rows_words = table.size();
+        table.resize(rows_words + (n_grp + n_seg + 1) / 2);
+        uint32_t* idx = reinterpret_cast<uint32_t*>(table.data() + rows_words);
+        memcpy(idx, grp_out.data(), n_grp * sizeof(uint32_t));
+        memcpy(idx + n_grp, seg_out.data(), n_seg * sizeof(uint32_t));
         uint64_t* d_table = nullptr;
         SNT_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_table), table.size() * sizeof(uint64_t), s));
         // pageable source: the call returns once the bytes sit in the driver's staging buffer
         cudaError_t e = cudaMemcpyAsync(d_table, table.data(), table.size() * sizeof(uint64_t), cudaMemcpyHostToDevice, s);
         if (e == cudaSuccess) {
-            const uint32_t* d_idx = reinterpret_cast<const uint32_t*>(reinterpret_cast<const uint8_t*>(d_table) + seg_bytes);
+            const uint64_t* d_grp = d_table;
+            const uint64_t* d_seg = d_table + grp_rows.size();
+            const uint32_t* d_grp_out = reinterpret_cast<const uint32_t*>(d_table + rows_words);
+            const uint32_t* d_seg_out = d_grp_out + n_grp;
             const uint8_t* empty = static_cast<const uint8_t*>(d_empty_digest);
+            uint8_t* work = static_cast<uint8_t*>(d_work);
             const MerkleConsts& c = node_consts();
-            const unsigned grid = static_cast<unsigned>(n_small);
+            const unsigned g_grid = static_cast<unsigned>(n_grp), s_grid = static_cast<unsigned>(n_seg);
             switch (alg) {
                 case SNT_SHA256:
-                    merkle_reduce_segments_kernel<ALG_SHA256, 256><<<grid, 256, 0, s>>>(in, d_table, d_idx, empty, c, out);
+                    if (n_grp) merkle_reduce_groups_kernel<ALG_SHA256, 256><<<g_grid, 256, 0, s>>>(d_grp, d_grp_out, c, work);
+                    merkle_reduce_segments_kernel<ALG_SHA256, 256><<<s_grid, 256, 0, s>>>(d_seg, d_seg_out, empty, c, out);
                     break;
                 case SNT_BLAKE2B:
-                    merkle_reduce_segments_kernel<ALG_BLAKE2B, 256><<<grid, 256, 0, s>>>(in, d_table, d_idx, empty, c, out);
+                    if (n_grp) merkle_reduce_groups_kernel<ALG_BLAKE2B, 256><<<g_grid, 256, 0, s>>>(d_grp, d_grp_out, c, work);
+                    merkle_reduce_segments_kernel<ALG_BLAKE2B, 256><<<s_grid, 256, 0, s>>>(d_seg, d_seg_out, empty, c, out);
                     break;
                 default:
-                    merkle_reduce_segments_kernel<ALG_SHA3_256, 256><<<grid, 256, 0, s>>>(in, d_table, d_idx, empty, c, out);
+                    if (n_grp) merkle_reduce_groups_kernel<ALG_SHA3_256, 256><<<g_grid, 256, 0, s>>>(d_grp, d_grp_out, c, work);
+                    merkle_reduce_segments_kernel<ALG_SHA3_256, 256><<<s_grid, 256, 0, s>>>(d_seg, d_seg_out, empty, c, out);
             }
             e = cudaGetLastError();
-            ++g_launches;
+            g_launches += n_grp ? 2 : 1;
         }
         cudaFreeAsync(d_table, s);
         if (e != cudaSuccess) return cuda_fail(e, "snt_merkle_roots_segmented");
-    }
-    for (uint32_t t = 0; t < n_segments; ++t) {
-        const uint64_t count = seg_first[t + 1] - seg_first[t];
-        if (count <= cta_cap) continue;
-        const int rc = snt_merkle_root(alg, in + seg_first[t] * dlen, count, d_work, work_bytes,
-                                       out + static_cast<size_t>(t) * dlen, stream);
-        if (rc != SNT_OK) return rc;
     }
     return SNT_OK;
 }

@@ -337,29 +337,52 @@ merkle_reduce_kernel(const uint8_t* __restrict__ in, uint64_t first, uint64_t n_
 }
 
 // One tree per segment (per_layer_hash, model.py:245-253), one CTA per segment, one launch for all
-// segments of at most 2^MAX_LEVELS digests: segment j covers digests [seg[2j], seg[2j] + seg[2j+1]) of
-// `in` and its root goes to out + seg_out[j] * DIGEST_BYTES. The root of a tree of `count` nodes under
+// segments of at most 2^MAX_LEVELS nodes: segment j covers the seg[2j+1] digests at ADDRESS seg[2j] (the leaf
+// digests of a small tensor, or the level-MAX_LEVELS nodes merkle_reduce_groups_kernel left in the workspace for a
+// large one) and its root goes to out + seg_out[j] * DIGEST_BYTES. The root of a tree of `count` nodes under
 // the reference rule (merkle.py:152-165) is the result of exactly ceil(log2(count)) levels; a single
 // digest is its own root and an empty segment takes the digest of the empty message.
 template <int ALG, int THREADS>
 __global__ void __launch_bounds__(THREADS)
-merkle_reduce_segments_kernel(const uint8_t* __restrict__ in, const uint64_t* __restrict__ seg,
-                              const uint32_t* __restrict__ seg_out, const uint8_t* __restrict__ empty_digest,
-                              const __grid_constant__ MerkleConsts c, uint8_t* __restrict__ out) {
+merkle_reduce_segments_kernel(const uint64_t* __restrict__ seg, const uint32_t* __restrict__ seg_out,
+                              const uint8_t* __restrict__ empty_digest, const __grid_constant__ MerkleConsts c,
+                              uint8_t* __restrict__ out) {
     using A = AlgTraits<ALG>;
     constexpr int CAP = ReduceShape<ALG>::CAP;
     __shared__ uint32_t buf_a[A::DW * CAP];
     __shared__ uint32_t buf_b[A::DW * CAP / 2];
-    const uint64_t begin = seg[2ull * blockIdx.x], count = seg[2ull * blockIdx.x + 1];
+    const uint8_t* in = reinterpret_cast<const uint8_t*>(seg[2ull * blockIdx.x]);
+    const uint64_t count = seg[2ull * blockIdx.x + 1];
     uint8_t* dst = out + static_cast<uint64_t>(seg_out[blockIdx.x]) * A::DIGEST_BYTES;
     if (count <= 1) {
-        const uint8_t* src = count ? in + begin * A::DIGEST_BYTES : empty_digest;
+        const uint8_t* src = count ? in : empty_digest;
         for (uint32_t i = threadIdx.x; i < A::DIGEST_BYTES; i += THREADS) dst[i] = src[i];
         return;
     }
     uint32_t levels = 0;
     while ((1ull << levels) < count) ++levels;
-    reduce_group<ALG, THREADS>(in + begin * A::DIGEST_BYTES, 0, count, 0, count, levels, 0, c, dst, buf_a, buf_b);
+    reduce_group<ALG, THREADS>(in, 0, count, 0, count, levels, 0, c, dst, buf_a, buf_b);
+}
+
+// The bottom MAX_LEVELS levels of MANY large trees in one launch: CTA r reduces group grp[3r+2] (2^MAX_LEVELS
+// aligned leaf digests) of the tree whose grp[3r+1] leaf digests start at ADDRESS grp[3r], and writes the
+// level-MAX_LEVELS node to out + grp_out[r] * DIGEST_BYTES. Same existence / zero-padding rule as everywhere
+// (reduce_group with the tree's own leaf count), so merkle_reduce_segments_kernel can finish every tree from
+// these nodes. Before: one chain of launches per large tensor, one after the other (GPT-2 small per-layer:
+// 26 tensors above 1,024 blocks, ~52 latency-bound launches, 2.4 ms for a 0.76 ms hash).
+template <int ALG, int THREADS>
+__global__ void __launch_bounds__(THREADS)
+merkle_reduce_groups_kernel(const uint64_t* __restrict__ grp, const uint32_t* __restrict__ grp_out,
+                            const __grid_constant__ MerkleConsts c, uint8_t* __restrict__ out) {
+    using A = AlgTraits<ALG>;
+    constexpr int CAP = ReduceShape<ALG>::CAP;
+    constexpr uint32_t LEVELS = ReduceShape<ALG>::MAX_LEVELS;
+    __shared__ uint32_t buf_a[A::DW * CAP];
+    __shared__ uint32_t buf_b[A::DW * CAP / 2];
+    const uint8_t* in = reinterpret_cast<const uint8_t*>(grp[3ull * blockIdx.x]);
+    const uint64_t count = grp[3ull * blockIdx.x + 1], group = grp[3ull * blockIdx.x + 2];
+    reduce_group<ALG, THREADS>(in, 0, count, group << LEVELS, count, LEVELS, 0, c,
+                               out + static_cast<uint64_t>(grp_out[blockIdx.x]) * A::DIGEST_BYTES, buf_a, buf_b);
 }
 
 }  // namespace snt

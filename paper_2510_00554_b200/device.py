@@ -554,8 +554,11 @@ def merkle_roots_segmented_device(alg: str, digests: torch.Tensor, seg_first: Se
     dev = require_cuda()
     dlen = DIGEST_LEN[alg]
     n_seg = len(seg_first) - 1
-    widest = max(b - a for a, b in zip(seg_first[:-1], seg_first[1:]))
-    wb = merkle_work_bytes(alg, max(widest, 1))
+    counts = [b - a for a, b in zip(seg_first[:-1], seg_first[1:])]
+    widest = max(counts)
+    # workspace: the reducer chain's buffers for the widest tree, or one node per 512 leaf digests of every large
+    # tree (the first launch of the segmented reducer leaves its level-9/10 nodes there), whichever is more
+    wb = max(merkle_work_bytes(alg, max(widest, 1)), sum(-(-c // 512) for c in counts if c > 512) * dlen)
     work = torch.empty(max(wb, 16), dtype=torch.uint8, device=dev)
     out = torch.empty(n_seg * dlen, dtype=torch.uint8, device=dev)
     first = (ctypes.c_uint64 * (n_seg + 1))(*seg_first)
