@@ -642,11 +642,29 @@ class LatticeAccumulator:
         _native.check(rc, "snt_lt_finalize")
         return out
 
-    def digests(self) -> Tuple[bytes, List[int], int]:
-        """(n_sources x 64 digest bytes, counts, status bits); synchronises."""
+    def finalize_to_host(self) -> None:
+        """Enqueue the read-out (no synchronisation): the finalize kernel stores the ``n_sources x 64`` digest bytes
+        straight into page-locked host memory through the unified address space, counts and status follow as one
+        asynchronous copy into the same block. ``host_result`` reads it after the stream has been synchronised."""
         lib = _native.load()
-        out = torch.empty(self.n_sources * 64, dtype=torch.uint8, device=self.acc.device)
-        rc = lib.snt_lt_finalize(_ptr(self.acc), self.n_sources, _ptr(out), _stream())
-        _native.check(rc, "snt_lt_finalize")
-        tail = self.state[self.n_sources * LT_LANES:].cpu().tolist()      # counts and status in one copy
-        return out.cpu().numpy().tobytes(), [int(c) for c in tail[:-1]], int(tail[-1])
+        n = self.n_sources
+        if self._out_host is None:
+            self._out_host = torch.empty(n * 64 + (n + 1) * 8, dtype=torch.uint8, pin_memory=True)
+        if lib.snt_device_reads_pinned_host():
+            rc = lib.snt_lt_finalize(_ptr(self.acc), n, _ptr(self._out_host), _stream())
+            _native.check(rc, "snt_lt_finalize")
+        else:
+            self._out_host[:n * 64].copy_(self.finalize_device(), non_blocking=True)
+        self._out_host[n * 64:].view(torch.int64).copy_(self.state[n * LT_LANES:], non_blocking=True)
+
+    def host_result(self) -> Tuple[bytes, List[int], int]:
+        n = self.n_sources
+        host = self._out_host.numpy()
+        tail = host[n * 64:].view(np.int64).tolist()
+        return host[:n * 64].tobytes(), [int(c) for c in tail[:-1]], int(tail[-1])
+
+    def digests(self) -> Tuple[bytes, List[int], int]:
+        """(n_sources x 64 digest bytes, counts, status bits); synchronises (once)."""
+        self.finalize_to_host()
+        torch.cuda.current_stream().synchronize()
+        return self.host_result()

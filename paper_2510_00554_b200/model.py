@@ -437,16 +437,26 @@ def _inplace_merkle_host(cfg: HashConfig, model: TensorMap, workers: int = 1) ->
 class _ResidentEntry:
     """Plan + workspace of one device-resident model: what a repeated ``hash_model`` call re-uses."""
 
-    __slots__ = ("key", "storages", "ids", "plan", "hasher", "host", "busy")
+    __slots__ = ("key", "storages", "ids", "plan", "hasher", "host", "busy", "acc")
 
-    def __init__(self, key, tensors, plan, hasher, host):
+    def __init__(self, key, tensors, plan, hasher, host, acc=None):
         self.key = key                   # (ptrs, sizes, block size, algorithm, device, stream)
         # the STORAGES the plan's addresses point into (not the tensor objects, which can be re-pointed with
         # `.data =` / `set_`): as long as the entry lives, a launch from the cached plan reads allocated memory
         self.storages = [t.untyped_storage() for t in tensors]
         self.ids = tuple(map(id, tensors))
         self.plan, self.hasher, self.host = plan, hasher, host
+        self.acc = acc                   # LATTICE construction: the accumulator instead of a Merkle hasher
         self.busy = threading.Lock()     # one call at a time owns the workspace
+
+    def launch(self) -> None:
+        """Enqueue the whole hash from the cached plan; the result lands in page-locked host memory."""
+        if self.hasher is not None:
+            self.hasher.run()
+        else:
+            self.acc.zero_()
+            self.acc.add_model_leaves(self.plan, 0, self.plan.leaf_count)
+            self.acc.finalize_to_host()
 
     def close(self) -> None:
         self.plan.close()
@@ -460,8 +470,8 @@ def _resident_key(buffers, cfg: HashConfig, stream):
     sizes = np.fromiter((b.nbytes for b in buffers), dtype=np.uint64, count=n)
     contiguous = all(b.is_cuda and b.is_contiguous() for b in buffers)   # `.data = cpu_tensor` moves a tensor object
     ptrs[sizes == 0] = 0
-    return (ptrs.tobytes(), sizes.tobytes(), cfg.block_size, cfg.alg.value, stream.device_index, stream.cuda_stream), \
-        ptrs, sizes, contiguous
+    return (ptrs.tobytes(), sizes.tobytes(), cfg.block_size, cfg.alg.value, cfg.construction.value, stream.device_index,
+            stream.cuda_stream), ptrs, sizes, contiguous
 
 
 def clear_hash_cache(model: Optional[TensorMap] = None) -> None:
@@ -492,9 +502,9 @@ def _inplace_merkle_resident(cfg: HashConfig, model: TensorMap, buffers=None) ->
     launched = False
     # O(1) checks only before the launch: the entry owns the storages its plan points into, so the speculative
     # launch is safe whatever the caller did to the TensorMap; WHICH tensors it holds now is checked afterwards
-    if entry is not None and entry.key[2:] == (cfg.block_size, cfg.alg.value, stream.device_index, stream.cuda_stream) \
-            and entry.busy.acquire(blocking=False):
-        entry.hasher.run()                                   # root lands in pinned host memory (host_out)
+    if entry is not None and entry.key[2:] == (cfg.block_size, cfg.alg.value, cfg.construction.value, stream.device_index,
+                                               stream.cuda_stream) and entry.busy.acquire(blocking=False):
+        entry.launch()                                       # the result lands in pinned host memory
         launched = True
     if buffers is None:
         buffers = [buf for _, buf in model.entries]
@@ -517,22 +527,29 @@ def _inplace_merkle_resident(cfg: HashConfig, model: TensorMap, buffers=None) ->
             return _inplace_merkle_uncached(cfg, buffers)
         plan = _dev.ModelPlan.from_spans([], ptrs, sizes, cfg.block_size, count=len(buffers))   # rejects an empty model
         try:
-            hasher = _dev.MerkleModelHasher(plan, cfg.alg.value, host_out=True)
+            if cfg.construction is Construction.MERKLE:
+                hasher, acc = _dev.MerkleModelHasher(plan, cfg.alg.value, host_out=True), None
+            else:
+                hasher, acc = None, _dev.LatticeAccumulator(1)
         except Exception:
             plan.close()
             raise
-        old, entry = entry, _ResidentEntry(key, list(buffers), plan, hasher, hasher.out)
+        old, entry = entry, _ResidentEntry(key, list(buffers), plan, hasher, hasher.out if hasher is not None else None, acc)
         entry.busy.acquire()
         model.__dict__["_resident"] = entry
         if old is not None:
             old.close()
-        entry.hasher.run()
+        entry.launch()
+    leaves = entry.plan.leaf_count
     try:
         stream.synchronize()
+        if entry.hasher is None:
+            out, _, _ = entry.acc.host_result()
+            # one 64-byte accumulator instead of the reference's n x 64 digest array
+            return ModelDigestResult(LatticeDigest(out), cfg, leaves, aux_digest_bytes=entry.acc.acc.numel() * 8)
         root = Digest(cfg.alg, entry.host.numpy().tobytes())
     finally:
         entry.busy.release()
-    leaves = entry.plan.leaf_count
     hasher = entry.hasher
     aux = hasher.leaves.numel() + hasher.work_bytes + (hasher.out.numel() if leaves > 1 else 0)
     return ModelDigestResult(root, cfg, leaves, aux_digest_bytes=aux)
@@ -548,11 +565,11 @@ def _inplace_merkle_uncached(cfg: HashConfig, buffers) -> ModelDigestResult:
 
 def inplace_hash(cfg: HashConfig, model: TensorMap, workers: int = 1) -> ModelDigestResult:
     """Hash fragmented tensors where they lie: no copy, no padding (model.py:298-315)."""
-    if cfg.construction is Construction.MERKLE and "_resident" in model.__dict__:
+    if "_resident" in model.__dict__:
         return _inplace_merkle_resident(cfg, model)          # launch first, re-check after
     buffers = [buf for _, buf in model.entries]
     all_resident = all(type(buf) is torch.Tensor and buf.is_cuda for buf in buffers)
-    if all_resident and buffers and cfg.construction is Construction.MERKLE:
+    if all_resident and buffers:
         return _inplace_merkle_resident(cfg, model, buffers)
     if not all_resident:
         _require_nonempty(model)

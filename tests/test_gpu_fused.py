@@ -255,6 +255,42 @@ def test_lthash_lanes_kernel_block_boundaries_and_alignments(dev, corc):
             assert dig.cpu().numpy().tobytes() == want_dig, (n, align, uniform)
 
 
+def test_resident_lattice_model_is_cached_and_revalidated(porc):
+    """LATTICE in-place hashing of device-resident tensors re-uses the plan and an accumulator whose read-out lands in
+    page-locked host memory; content changes, re-pointed tensors and a change of construction on the same TensorMap
+    all give the oracle's answer."""
+    import paper_2510_00554_b200 as pkg
+
+    rng = np.random.default_rng(8)
+    sizes = [8192 * 20 + 5, 100, 8192 * 64, 0, 7]
+    host = [rng.integers(0, 256, size=s, dtype=np.uint8) for s in sizes]
+    tensors = [torch.from_numpy(h).cuda() for h in host]
+    model = pkg.TensorMap([(f"t{i}", t) for i, t in enumerate(tensors)])
+    lat = pkg.HashConfig(pkg.Construction.LATTICE, pkg.Strategy.IN_PLACE, pkg.CompressionAlg.BLAKE2B)
+    mer = pkg.HashConfig(pkg.Construction.MERKLE, pkg.Strategy.IN_PLACE, pkg.CompressionAlg.BLAKE2B)
+
+    def want_lat():
+        return porc.inplace_lattice([h.tobytes() for h in host], 8192)
+
+    assert pkg.hash_model(lat, model).model_digest.data == want_lat()
+    entry = model.__dict__["_resident"]
+    assert entry.acc is not None and entry.hasher is None
+    assert pkg.hash_model(lat, model).model_digest.data == want_lat()
+    assert model.__dict__["_resident"] is entry
+    host[2][777] ^= 0x55
+    tensors[2][777] ^= 0x55
+    assert pkg.hash_model(lat, model).model_digest.data == want_lat()
+    assert model.__dict__["_resident"] is entry
+    host[1] = rng.integers(0, 256, size=100, dtype=np.uint8)
+    tensors[1].data = torch.from_numpy(host[1]).cuda()
+    assert pkg.hash_model(lat, model).model_digest.data == want_lat()
+    assert model.__dict__["_resident"] is not entry
+    # the other construction on the same TensorMap: a new entry, then back again
+    assert pkg.hash_model(mer, model).model_digest.data == porc.inplace_merkle("blake2b", [h.tobytes() for h in host], 8192)
+    assert model.__dict__["_resident"].hasher is not None
+    assert pkg.hash_model(lat, model).model_digest.data == want_lat()
+
+
 def test_resident_model_tiny_trees_root_lands_in_pinned_host_memory(porc):
     """One- and two-leaf device-resident models through the cached path, whose output buffer is page-locked HOST memory
     (the last kernel -- or, for a single leaf, an asynchronous device-to-host copy of the leaf digest -- writes the root
