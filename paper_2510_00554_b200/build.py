@@ -2,6 +2,8 @@
 
 * ``lib/libsentinel_b200.so`` -- the sm_100a kernels plus the C ABI declared
   in ``include/sentinel_b200.h``.
+* ``_hostpack.so`` -- CPython helper (plain C) that packs sequences of host blocks / sample records
+  into page-locked memory for the reference-shaped entry points (no hashing in it).
 * ``oracle/_build/liboracle.so`` -- the plain-C CPU restatement used by the
   tests and by ``bench.py``'s CPU baseline (test infrastructure, never loaded
   by this package).
@@ -25,6 +27,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB_DIR = PKG / "lib"
 LIB_PATH = LIB_DIR / "libsentinel_b200.so"
+HOSTPACK_LIB = PKG / "_hostpack.so"
 ORACLE_DIR = ROOT / "oracle"
 ORACLE_LIB = ORACLE_DIR / "_build" / "liboracle.so"
 HOSTCHECK_DIR = ROOT / "tests" / "hostcheck"
@@ -67,6 +70,16 @@ def build_native(force: bool = False) -> Path:
     LIB_DIR.mkdir(parents=True, exist_ok=True)
     _run([_nvcc(), *NVCC_FLAGS, "-shared", *sorted(CSRC.glob("*.cu")), "-o", LIB_PATH])
     return LIB_PATH
+
+
+def build_hostpack(force: bool = False) -> Path:
+    import sysconfig
+    src = CSRC / "hostpack.c"
+    if not force and _newer(HOSTPACK_LIB, [src]):
+        return HOSTPACK_LIB
+    _run(["gcc", "-O2", "-std=c11", "-fPIC", "-shared", "-pthread", "-Wall",
+          "-I" + sysconfig.get_paths()["include"], src, "-o", HOSTPACK_LIB])
+    return HOSTPACK_LIB
 
 
 def build_oracle(force: bool = False) -> Path:
@@ -129,6 +142,7 @@ def stage_reference(force: bool = False) -> Path:
 
 def build_all(force: bool = False) -> None:
     build_native(force)
+    build_hostpack(force)
     stage_reference(force)
     if (ORACLE_DIR / "oracle.c").exists():
         build_oracle(force)

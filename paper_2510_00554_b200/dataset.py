@@ -112,6 +112,7 @@ class _BatchEngine:
         self.turn = 0
         self.d_block: Optional[torch.Tensor] = None
         self.pending = False
+        self._last_need = 0
 
     def _slot(self, sid: int) -> int:
         slot = self.slot_of.get(sid)
@@ -127,12 +128,8 @@ class _BatchEngine:
             self.slot_of[sid] = slot
         return slot
 
-    def add(self, payloads: Sequence[bytes], ids: np.ndarray, source_ids: Sequence[int]) -> None:
-        n = len(payloads)
-        lengths = np.fromiter(map(len, payloads), dtype=np.uint64, count=n)
-        total = int(lengths.sum())
-        header = -(-28 * n // self.HEADER_ALIGN) * self.HEADER_ALIGN
-        need = header + max(total, 16)
+    def _stage_for(self, need: int) -> Tuple[int, torch.Tensor]:
+        """A staging block of at least ``need`` bytes whose last transfer has completed, and its index."""
         turn = self.turn
         self.turn ^= 1
         if self.stage[turn] is None or self.stage[turn].numel() < need:
@@ -142,7 +139,56 @@ class _BatchEngine:
             self.stage_done[turn].synchronize()            # the copy that last read this staging buffer
         if self.d_block is None or self.d_block.numel() < need:
             self.d_block = torch.empty(max(need * 2, 1 << 20), dtype=torch.uint8, device=self.device)
-        view = self.stage[turn].numpy()
+        return turn, self.stage[turn]
+
+    def _launch(self, turn: int, n: int, header: int, need: int, uniform: bool) -> None:
+        d = self.d_block
+        d[:need].copy_(self.stage[turn][:need], non_blocking=True)
+        done = torch.cuda.Event()
+        done.record()
+        self.stage_done[turn] = done
+        self.acc.add_packed(d, n, header, uniform=uniform)
+        self.pending = True
+
+    def add_records(self, samples: Sequence[SampleRecord], cover_labels: bool, declared: Optional[frozenset]) -> bool:
+        """Pack the records with the C helper (one pass: checks, header, payload bytes straight into the pinned
+        block) and launch. False when the helper is not built; the checks raise what ``process_batch`` raises."""
+        pack = _dev._hostpack
+        if pack is None:
+            return False
+        n = len(samples)
+        turn, stage = self._stage_for(max(self._last_need, 1 << 20))
+        while True:
+            code, a, b = pack.pack_records(samples, cover_labels, self.slot_of, declared, stage.data_ptr(), stage.numel())
+            if code == 0:
+                break
+            if code == 1:                                   # block too small: grow it and pack again
+                self.turn ^= 1
+                turn, stage = self._stage_for(a)
+            elif code == 2:
+                s = samples[a]
+                raise ValidationError(f"sample {s.sample_id} references undeclared source {s.source_id}")
+            elif code == 3:
+                raise ValidationError(f"sample id {samples[a].sample_id} does not fit an unsigned 64-bit tag")
+            else:                                           # a source seen for the first time
+                self._slot(samples[a].source_id)
+        total, header = a, b
+        need = header + max(total, 16)
+        self._last_need = need
+        if self.d_block.numel() < need:
+            self.d_block = torch.empty(need * 2, dtype=torch.uint8, device=self.device)
+        lens = stage[8 * n:16 * n].numpy().view(np.uint64)
+        self._launch(turn, n, header, need, _all_equal(lens))
+        return True
+
+    def add(self, payloads: Sequence[bytes], ids: np.ndarray, source_ids: Sequence[int]) -> None:
+        n = len(payloads)
+        lengths = np.fromiter(map(len, payloads), dtype=np.uint64, count=n)
+        total = int(lengths.sum())
+        header = -(-28 * n // self.HEADER_ALIGN) * self.HEADER_ALIGN
+        need = header + max(total, 16)
+        turn, stage = self._stage_for(need)
+        view = stage.numpy()
         offsets = view[0:8 * n].view(np.uint64)
         offsets[0] = 0
         np.cumsum(lengths[:-1], out=offsets[1:])
@@ -154,15 +200,7 @@ class _BatchEngine:
             slots = [self._slot(s) for s in source_ids]
         view[24 * n:28 * n].view(np.int32)[:] = slots
         view[header:header + total] = np.frombuffer(b"".join(payloads), dtype=np.uint8)
-        d = self.d_block
-        d[:need].copy_(self.stage[turn][:need], non_blocking=True)
-        done = torch.cuda.Event()
-        done.record()
-        self.stage_done[turn] = done
-        self.acc.add_samples(d[header:], d[0:8 * n].view(torch.int64), d[8 * n:16 * n].view(torch.int64),
-                             d[16 * n:24 * n].view(torch.int64), d[24 * n:28 * n].view(torch.int32),
-                             uniform=_all_equal(lengths))
-        self.pending = True
+        self._launch(turn, n, header, need, _all_equal(lengths))
 
     def drain(self) -> Dict[int, Tuple[bytes, int]]:
         """Per-source (64 digest bytes, count) accumulated since the last drain; synchronises, then starts from zero."""
@@ -330,6 +368,11 @@ def process_batch(batch: Batch, acc: SourceAccumulator) -> SourceAccumulator:
     host-side ``acc.sums`` / ``acc.counts`` catch up when they are read (``finalize`` does).
     """
     samples = batch.samples
+    if samples and _dev._hostpack is not None:
+        if acc._engine is None:
+            acc._engine = _BatchEngine()
+        acc._engine.add_records(samples, acc.cover_labels, acc.declared_sources)
+        return acc
     source_ids = [s.source_id for s in samples]
     if acc.declared_sources is not None and not acc.declared_sources.issuperset(source_ids):
         s = next(s for s in samples if s.source_id not in acc.declared_sources)

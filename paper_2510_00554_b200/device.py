@@ -20,6 +20,11 @@ import torch
 from . import _native
 from .errors import InvalidInput, ResourceError
 
+try:                                    # CPython helper built next to the CUDA library (build.build_hostpack)
+    from . import _hostpack
+except ImportError:                     # only the packing gets slower; hashing never runs on the host either way
+    _hostpack = None
+
 ALG_IDS = {"sha256": 0, "blake2b": 1, "sha3-256": 2}
 DIGEST_LEN = {"sha256": 32, "blake2b": 64, "sha3-256": 32}
 LT_LANES = 32
@@ -79,6 +84,51 @@ def as_device_bytes(buf, device: Optional[torch.device] = None) -> torch.Tensor:
         warnings.simplefilter("ignore")          # read-only buffers are only read
         host = torch.from_numpy(arr)
     return host.to(device, non_blocking=True)
+
+
+class PinnedPack:
+    """One reused page-locked block that sequences of host blocks are gathered into (``_hostpack.gather``),
+    then copied to the device with one asynchronous transfer. The block is reused once the transfer that
+    last read it has completed."""
+
+    MAX_BYTES = 2 << 30                 # larger packs take the staging ring (bounded pinned memory)
+    _local = threading.local()
+
+    @classmethod
+    def get(cls) -> "PinnedPack":
+        inst = getattr(cls._local, "inst", None)
+        if inst is None:
+            inst = cls._local.inst = cls()
+        return inst
+
+    def __init__(self):
+        self.block: Optional[torch.Tensor] = None
+        self.done: Optional[torch.cuda.Event] = None
+
+    def to_device(self, blocks: Sequence, device: torch.device) -> Optional[Tuple[torch.Tensor, np.ndarray]]:
+        """(device bytes, u64 lengths) of the blocks laid back to back, or None when the helper cannot take
+        them (not built, an item without a contiguous buffer, a pack above ``MAX_BYTES``)."""
+        if _hostpack is None:
+            return None
+        lens = np.empty(len(blocks), dtype=np.uint64)
+        try:
+            total = _hostpack.gather(blocks, 0, 0, lens.ctypes.data)
+        except (TypeError, BufferError, ValueError):
+            return None
+        if total > self.MAX_BYTES:
+            return None
+        if total == 0:
+            return torch.zeros(16, dtype=torch.uint8, device=device), lens
+        if self.done is not None:
+            self.done.synchronize()
+        if self.block is None or self.block.numel() < total:
+            self.block = torch.empty(max(total, 1 << 20), dtype=torch.uint8, pin_memory=True)
+        _hostpack.gather(blocks, self.block.data_ptr(), total, 0)
+        out = torch.empty(total, dtype=torch.uint8, device=device)
+        out.copy_(self.block[:total], non_blocking=True)
+        self.done = torch.cuda.Event()
+        self.done.record()
+        return out, lens
 
 
 STAGE_RING_SLOTS = 4
@@ -603,6 +653,19 @@ class LatticeAccumulator:
         shape = _native.SAMPLES_UNKNOWN if uniform is None else (_native.SAMPLES_UNIFORM if uniform else _native.SAMPLES_RAGGED)
         rc = lib.snt_lthash_samples_shaped(_ptr(shard), _ptr(offsets), _ptr(lengths), _ptr(ids), _ptr(slots), n,
                                            self.n_sources, _ptr(self.acc), _ptr(self.counts), _ptr(digests),
+                                           _ptr(self.status), shape, _stream())
+        _native.check(rc, "snt_lthash_samples_shaped")
+
+    def add_packed(self, block: torch.Tensor, n: int, header: int, uniform: Optional[bool] = None) -> None:
+        """A batch in the one-block layout ``offsets[n] u64 | lengths[n] u64 | ids[n] u64 | slots[n] i32 | pad |
+        sample bytes (from byte ``header``)`` -- what ``process_batch`` ships per batch; addresses by arithmetic,
+        no tensor views."""
+        lib = _native.load()
+        base = block.data_ptr()
+        shape = _native.SAMPLES_UNKNOWN if uniform is None else (_native.SAMPLES_UNIFORM if uniform else _native.SAMPLES_RAGGED)
+        vp = ctypes.c_void_p
+        rc = lib.snt_lthash_samples_shaped(vp(base + header), vp(base), vp(base + 8 * n), vp(base + 16 * n), vp(base + 24 * n),
+                                           n, self.n_sources, _ptr(self.acc), _ptr(self.counts), None,
                                            _ptr(self.status), shape, _stream())
         _native.check(rc, "snt_lthash_samples_shaped")
 

@@ -98,15 +98,21 @@ def _stage_blocks(blocks: Sequence):
         lens = np.array([t.numel() for t in keep], dtype=np.uint64)
         base = None
     else:
-        views = [_dev.host_bytes_view(b.cpu().numpy() if isinstance(b, torch.Tensor) else b) for b in blocks]
-        lens = np.fromiter((v.size for v in views), dtype=np.uint64, count=n)
+        host = [b.cpu().numpy() if isinstance(b, torch.Tensor) else b for b in blocks] \
+            if any(isinstance(b, torch.Tensor) for b in blocks) else blocks
+        packed = _dev.PinnedPack.get().to_device(host, dev)      # one C pass over the buffers into pinned memory
+        if packed is not None:
+            base, lens = packed
+        else:
+            views = [_dev.host_bytes_view(b) for b in host]
+            lens = np.fromiter((v.size for v in views), dtype=np.uint64, count=n)
+            total = int(lens.sum())
+            flat = np.concatenate(views) if total else np.zeros(0, dtype=np.uint8)
+            # (large packs travel through the pinned staging ring: ~50 GB/s instead of a pageable cudaMemcpy's ~10)
+            base = _dev.as_device_bytes(flat, dev) if total else torch.zeros(16, dtype=torch.uint8, device=dev)
         offs = np.zeros(n, dtype=np.uint64)
         if n > 1:
             np.cumsum(lens[:-1], out=offs[1:])
-        total = int(lens.sum())
-        packed = np.concatenate(views) if total else np.zeros(0, dtype=np.uint8)
-        # (large packs travel through the pinned staging ring: ~50 GB/s instead of a pageable cudaMemcpy's ~10)
-        base = _dev.as_device_bytes(packed, dev) if total else torch.zeros(16, dtype=torch.uint8, device=dev)
         keep = [base]
     d_off = torch.from_numpy(offs.view(np.int64)).to(dev)
     d_len = torch.from_numpy(lens.view(np.int64)).to(dev)
