@@ -559,8 +559,9 @@ int launch_lthash_lanes(const Items& items, uint64_t n, uint32_t n_sources, unsi
         static_cast<int>(LTL_MAXW * ltl_warp_bytes(Items::TAG_WORDS) + acc_max));
     if (attr != cudaSuccess) return cuda_fail(attr, "cudaFuncSetAttribute(lthash_lanes_kernel)");
     const uint64_t sms = static_cast<uint64_t>(sm_count());
-    // at least one item per lane, a multiple of four warps per CTA, at most three per scheduler
-    int warps = static_cast<int>((n / (sms * 32)) & ~3ull);
+    // at least two items per lane (a lane that holds one sample cannot even out the ragged lengths: 40 k samples
+    // 61.7 us at 8 warps, 57.8 at 4), a multiple of four warps per CTA, at most three per scheduler
+    int warps = static_cast<int>((n / (sms * 64)) & ~3ull);
     if (const char* force = getenv("SNT_LT_LANES_WARPS")) warps = atoi(force);
     warps = warps < 4 ? 4 : (warps > LTL_MAXW ? LTL_MAXW : warps);
     const uint64_t want_ctas = (n + static_cast<uint64_t>(warps) * 32 - 1) / (static_cast<uint64_t>(warps) * 32);

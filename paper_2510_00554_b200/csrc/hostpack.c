@@ -219,7 +219,47 @@ done:
     return result;
 }
 
+/* manifest_columns(rows, ids_addr, src_addr, off_addr, len_addr) -> (code, index)
+ *
+ * rows: sequence of (sample_id, source_id, label, offset, length) tuples (DatasetManifest.samples). Writes the
+ * four integer columns (u64 ids, i64 the rest) in one pass.
+ *   (0, n)      done
+ *   (3, index)  rows[index].sample_id does not fit an unsigned 64-bit tag
+ *   (5, index)  another field of rows[index] is not an integer that fits 64 bits (caller takes its Python path) */
+static PyObject *hp_manifest_columns(PyObject *self, PyObject *args) {
+    PyObject *seq_in;
+    unsigned long long a_ids, a_src, a_off, a_len;
+    if (!PyArg_ParseTuple(args, "OKKKK", &seq_in, &a_ids, &a_src, &a_off, &a_len)) return NULL;
+    PyObject *seq = PySequence_Fast(seq_in, "manifest_columns expects a sequence of rows");
+    if (!seq) return NULL;
+    size_t n = (size_t)PySequence_Fast_GET_SIZE(seq);
+    PyObject **items = PySequence_Fast_ITEMS(seq);
+    uint64_t *ids = (uint64_t *)(uintptr_t)a_ids;
+    int64_t *cols[3] = {(int64_t *)(uintptr_t)a_src, (int64_t *)(uintptr_t)a_off, (int64_t *)(uintptr_t)a_len};
+    static const int field[3] = {1, 3, 4};
+    long code = 0; size_t at = n;
+    for (size_t i = 0; i < n && !code; ++i) {
+        PyObject *row = items[i];
+        if (!PyTuple_Check(row) || PyTuple_GET_SIZE(row) < 5) { code = 5; at = i; break; }
+        PyObject *idobj = PyTuple_GET_ITEM(row, 0);
+        if (!PyLong_Check(idobj)) { code = 3; at = i; break; }
+        unsigned long long id = PyLong_AsUnsignedLongLong(idobj);
+        if (id == (unsigned long long)-1 && PyErr_Occurred()) { PyErr_Clear(); code = 3; at = i; break; }
+        ids[i] = id;
+        for (int c = 0; c < 3; ++c) {
+            PyObject *v = PyTuple_GET_ITEM(row, field[c]);
+            long long x = PyLong_Check(v) ? PyLong_AsLongLong(v) : -1;
+            if (!PyLong_Check(v) || (x == -1 && PyErr_Occurred())) { PyErr_Clear(); code = 5; at = i; break; }
+            cols[c][i] = x;
+        }
+    }
+    Py_DECREF(seq);
+    return Py_BuildValue("(ln)", code, (Py_ssize_t)at);
+}
+
 static PyMethodDef methods[] = {
+    {"manifest_columns", hp_manifest_columns, METH_VARARGS,
+     "manifest_columns(rows, ids_addr, src_addr, off_addr, len_addr) -> (code, index)"},
     {"gather", hp_gather, METH_VARARGS, "gather(seq, dst_addr, capacity, lens_addr, threads=8) -> total bytes"},
     {"pack_records", hp_pack_records, METH_VARARGS,
      "pack_records(samples, cover_labels, slot_of, declared, dst_addr, capacity) -> (code, a, b)"},

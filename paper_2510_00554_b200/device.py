@@ -211,7 +211,16 @@ class RingWriter:
 
     def write(self, off: int, src: np.ndarray) -> None:
         """Queue the copy of flat uint8 ``src`` to ``dst[off : off + len(src)]``."""
-        n, pos = int(src.shape[0]), 0
+        self._write(off, int(src.shape[0]), lambda view, p0, p1: np.copyto(view, src[p0:p1]))
+
+    def write_file(self, off: int, fd: int, file_off: int, n: int) -> None:
+        """Queue ``n`` bytes of the open file ``fd`` from ``file_off`` to ``dst[off : off + n]``: the staging threads
+        ``pread`` straight into the pinned buffers (one copy out of the page cache, none through a ``bytes`` object)."""
+        self._write(off, n, lambda view, p0, p1: _pread_exact(fd, view, file_off + p0))
+
+    def _write(self, off: int, n: int, copy) -> None:
+        """``copy(view, p0, p1)`` fills the pinned ``view`` with source bytes [p0, p1); it runs on the pool for large pieces."""
+        pos = 0
         ring = self.ring
         while pos < n:
             if self.slot < 0:
@@ -225,11 +234,11 @@ class RingWriter:
             if so > self.fill:
                 view[self.fill:so] = 0                      # alignment gap between two buffers: defined bytes
             if take < STAGE_INLINE_MAX_BYTES:               # a task costs more than a small memcpy
-                np.copyto(view[so:so + take], src[pos:pos + take])
+                copy(view[so:so + take], pos, pos + take)
             else:
                 for p0 in range(0, take, STAGE_PIECE_BYTES):
                     p1 = min(take, p0 + STAGE_PIECE_BYTES)
-                    self.tasks.append(ring.pool.submit(np.copyto, view[so + p0:so + p1], src[pos + p0:pos + p1]))
+                    self.tasks.append(ring.pool.submit(copy, view[so + p0:so + p1], pos + p0, pos + p1))
             self.fill = so + take
             pos += take
             if self.fill >= STAGE_SLOT_BYTES:
@@ -275,6 +284,44 @@ def pageable_to_device(src: np.ndarray, dst: torch.Tensor, workers: int = 1) -> 
         w.write(0, src)
         w.drain()
         stream.synchronize()      # the ring may be handed to another caller / stream after the lock is released
+
+
+def _pread_exact(fd: int, view: np.ndarray, file_off: int) -> None:
+    import os
+
+    mv, got = memoryview(view), 0
+    while got < len(mv):
+        r = os.preadv(fd, [mv[got:]], file_off + got)
+        if r <= 0:
+            raise OSError(f"short read at byte {file_off + got}")
+        got += r
+
+
+def file_to_device(path, device: Optional[torch.device] = None, workers: int = 1) -> torch.Tensor:
+    """The bytes of a file as a flat uint8 CUDA tensor. Large files are read by the staging threads straight into
+    the pinned ring and transferred buffer by buffer while the next one is being read (``read_bytes`` + copy of a
+    150 MB shard: 59 + 7 ms; this: one pass at the speed of the page cache). Raises ``OSError`` like ``open``/``read``."""
+    import os
+
+    device = device or require_cuda()
+    with open(path, "rb", buffering=0) as f:
+        size = os.fstat(f.fileno()).st_size
+        if size < STAGE_DIRECT_MAX_BYTES:
+            return as_device_bytes(f.read(), device)
+        out = torch.empty(size, dtype=torch.uint8, device=device)
+        ring = StagingRing.get(staging_threads(workers))
+        stream = torch.cuda.current_stream()
+        with ring.lock:
+            w = RingWriter(ring, out, stream)
+            try:
+                w.write_file(0, f.fileno(), 0, size)
+                w.drain()
+            finally:
+                for item in list(w.pending) + [(0, 0, 0, w.tasks)]:      # no task may outlive the file descriptor
+                    for t in item[3]:
+                        t.exception()
+                stream.synchronize()
+    return out
 
 
 ARENA_ALIGN = 256

@@ -97,3 +97,18 @@ def test_pack_records_status_codes():
     assert (code, needed) == (1, 32 + 16)
     assert not dst.any()
     assert _hostpack.pack_records([], False, slot_of, None, *args) == (0, 0, 0)
+
+
+def test_manifest_columns():
+    rows = [(5, 1, b"a", 0, 10), ((1 << 64) - 1, -3, b"", 7, 0), (0, 2, b"zz", 1 << 40, 3)]
+    ids = np.zeros(3, dtype=np.uint64)
+    src, off, ln = (np.zeros(3, dtype=np.int64) for _ in range(3))
+    ptrs = (ids.ctypes.data, src.ctypes.data, off.ctypes.data, ln.ctypes.data)
+    assert _hostpack.manifest_columns(rows, *ptrs) == (0, 3)
+    assert ids.tolist() == [5, (1 << 64) - 1, 0] and src.tolist() == [1, -3, 2]
+    assert off.tolist() == [0, 7, 1 << 40] and ln.tolist() == [10, 0, 3]
+    assert _hostpack.manifest_columns([(1, 1, b"", 0, 1), (-1, 1, b"", 0, 1)], *ptrs) == (3, 1)
+    assert _hostpack.manifest_columns([(1 << 64, 1, b"", 0, 1)], *ptrs) == (3, 0)
+    assert _hostpack.manifest_columns([(1, 1, b"", 1 << 70, 1)], *ptrs) == (5, 0)      # caller's Python path decides
+    assert _hostpack.manifest_columns([[1, 1, b"", 0, 1]], *ptrs) == (5, 0)            # not a tuple
+    assert _hostpack.manifest_columns([], *ptrs) == (0, 0)

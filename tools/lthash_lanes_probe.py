@@ -61,7 +61,7 @@ def main():
         ds = dsm.DeviceDataset.from_host(shard, offs, lens, ids, src, list(range(n_src)))
         acc = dev.LatticeAccumulator(n_src)
         variants = [("grid", _native.SCHEDULE_GRID, None), ("chains", _native.SCHEDULE_FUSED, None)]
-        variants += [(f"lanes_w{w}", _native.SCHEDULE_PERSISTENT, w) for w in (8, 12, 16)]
+        variants += [(f"lanes_w{w}", _native.SCHEDULE_PERSISTENT, w) for w in (4, 8, 12, 16)]
         variants += [("lanes_auto", _native.SCHEDULE_PERSISTENT, 0)]
         ref = None
         for vname, sched, w in variants:
