@@ -862,3 +862,69 @@ def test_tensor_larger_than_4_gib(pkg, corc):
     lat = pkg.HashConfig(pkg.Construction.LATTICE, pkg.Strategy.IN_PLACE, pkg.CompressionAlg.BLAKE2B)
     got = pkg.hash_model(lat, pkg.TensorMap([(f"t{i}", p) for i, p in enumerate(parts)]))
     assert got.model_digest.data == corc.inplace_lattice(tl, 8192, threads)
+
+
+@pytest.mark.parametrize("cover_labels", [False, True])
+def test_digest_dataset_large_shard_file_with_gaps_and_labels(pkg, porc, tmp_path, cover_labels):
+    """digest_dataset on a shard FILE above the direct-copy threshold (read by the staging threads into the pinned
+    ring), rows in shuffled order with gaps between samples, empty samples, labels of 0-11 bytes laid out by the
+    device gather; every per-source digest and count against the oracle (dataset.py:41-49, :166-195)."""
+    rng = np.random.default_rng(11)
+    n, n_src = 6000, 7
+    lens = rng.integers(0, 4200, size=n)
+    lens[rng.integers(0, n, size=40)] = 0
+    gaps = rng.integers(0, 9, size=n)
+    offs = np.cumsum(lens + gaps) - lens
+    shard = rng.integers(0, 256, size=int(offs[-1] + lens[-1]) + 5, dtype=np.uint8).tobytes()
+    assert len(shard) > (8 << 20)
+    labels = [bytes(rng.integers(97, 123, size=int(k), dtype=np.uint8)) for k in rng.integers(0, 12, size=n)]
+    ids = rng.integers(0, 1 << 63, size=n, dtype=np.uint64) * 2 + rng.integers(0, 2, size=n, dtype=np.uint64)
+    src = rng.integers(10, 10 + n_src, size=n)
+    order = rng.permutation(n)
+    rows = [(int(ids[i]), int(src[i]), labels[i], int(offs[i]), int(lens[i])) for i in order]
+    man = pkg.DatasetManifest(rows, tmp_path / "big.bin")
+    (tmp_path / "big.bin").write_bytes(shard)
+    want = porc.dataset_digests(((sid, s, lab, shard[o:o + ln]) for sid, s, lab, o, ln in rows), cover_labels=cover_labels)
+    got = pkg.digest_dataset(man, cover_labels=cover_labels)
+    assert {k: (d.data, c) for k, (d, c) in got.items()} == want
+    # a row that runs past the end of the file is a FormatError, as in the reference
+    bad = pkg.DatasetManifest(rows + [(1, 10, b"", len(shard) - 3, 4)], tmp_path / "big.bin")
+    with pytest.raises(pkg.errors.FormatError):
+        pkg.digest_dataset(bad, cover_labels=cover_labels)
+    with pytest.raises(pkg.errors.FormatError):
+        pkg.digest_dataset(pkg.DatasetManifest(rows, tmp_path / "missing.bin"))
+
+
+def test_process_batch_helper_and_python_packer_agree(pkg):
+    """process_batch through the C packer (_hostpack.pack_records) and through the Python packer: same sums, and the
+    same errors in the same order (undeclared source before a bad id)."""
+    from paper_2510_00554_b200 import device as dev
+
+    rng = np.random.default_rng(5)
+    recs = [pkg.SampleRecord(int(rng.integers(0, 1 << 62)), int(rng.integers(0, 40)), b"L%d" % (i % 3),
+                             bytes(rng.integers(0, 256, size=int(rng.integers(0, 700)), dtype=np.uint8))) for i in range(1000)]
+    assert dev._hostpack is not None, "the packing helper must be built in-tree (build.build_hostpack)"
+
+    def run(cover):
+        acc = pkg.SourceAccumulator(cover_labels=cover)
+        for s in range(0, len(recs), 128):
+            pkg.process_batch(pkg.Batch(recs[s:s + 128]), acc)
+        return {k: (d.data, c) for k, (d, c) in pkg.finalize(acc).items()}
+
+    helper = dev._hostpack
+    try:
+        for cover in (False, True):
+            with_c = run(cover)
+            dev._hostpack = None
+            assert run(cover) == with_c
+            dev._hostpack = helper
+        for packer in (helper, None):
+            dev._hostpack = packer
+            acc = pkg.SourceAccumulator()
+            acc.declare([1])
+            with pytest.raises(pkg.errors.ValidationError, match="undeclared source 9"):
+                pkg.process_batch(pkg.Batch([pkg.SampleRecord(-5, 1, b"", b"x"), pkg.SampleRecord(3, 9, b"", b"y")]), acc)
+            with pytest.raises(pkg.errors.ValidationError, match="64-bit"):
+                pkg.process_batch(pkg.Batch([pkg.SampleRecord(1 << 64, 1, b"", b"x")]), acc)
+    finally:
+        dev._hostpack = helper
