@@ -90,6 +90,14 @@ def hash_sample(s: SampleRecord, cover_labels: bool = False) -> LatticeDigest:
     return lt_hash_block(s.sample_id, s.data)
 
 
+def _raise_record_error(code: int, s: "SampleRecord") -> None:
+    """The check codes of ``_hostpack.pack_records`` as the exceptions ``process_batch`` raises."""
+    if code == 2:
+        raise ValidationError(f"sample {s.sample_id} references undeclared source {s.source_id}")
+    if code == 3:
+        raise ValidationError(f"sample id {s.sample_id} does not fit an unsigned 64-bit tag")
+
+
 class _BatchEngine:
     """Device side of a ``SourceAccumulator`` that is fed batch by batch (``process_batch``).
 
@@ -165,13 +173,10 @@ class _BatchEngine:
             if code == 1:                                   # block too small: grow it and pack again
                 self.turn ^= 1
                 turn, stage = self._stage_for(a)
-            elif code == 2:
-                s = samples[a]
-                raise ValidationError(f"sample {s.sample_id} references undeclared source {s.source_id}")
-            elif code == 3:
-                raise ValidationError(f"sample id {samples[a].sample_id} does not fit an unsigned 64-bit tag")
-            else:                                           # a source seen for the first time
+            elif code == 4:                                 # a source seen for the first time
                 self._slot(samples[a].source_id)
+            else:
+                _raise_record_error(code, samples[a])
         total, header = a, b
         need = header + max(total, 16)
         self._last_need = need
@@ -370,6 +375,9 @@ def process_batch(batch: Batch, acc: SourceAccumulator) -> SourceAccumulator:
     samples = batch.samples
     if samples and _dev._hostpack is not None:
         if acc._engine is None:
+            # first batch: the checks alone (no destination), so that a bad batch raises before anything touches the device
+            code, at, _ = _dev._hostpack.pack_records(samples, acc.cover_labels, {}, acc.declared_sources, 0, 0)
+            _raise_record_error(code, samples[at] if code in (2, 3) else None)
             acc._engine = _BatchEngine()
         acc._engine.add_records(samples, acc.cover_labels, acc.declared_sources)
         return acc
