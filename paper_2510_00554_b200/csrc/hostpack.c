@@ -13,6 +13,7 @@
 #include <Python.h>
 #include <pthread.h>
 #include <stdint.h>
+#include <stdlib.h>
 #include <string.h>
 
 typedef struct {
@@ -257,7 +258,251 @@ static PyObject *hp_manifest_columns(PyObject *self, PyObject *args) {
     return Py_BuildValue("(ln)", code, (Py_ssize_t)at);
 }
 
+/* ---- a persistent pool of copy threads ---------------------------------------------------------------------------
+ * Fills pinned staging buffers from pageable memory (streaming stores) or from a file (pread). The Python version
+ * queued one task per 4 MB piece on a ThreadPoolExecutor and copied with ordinary stores. Here the threads live in C,
+ * take 1 MB jobs from a queue of batches and never touch the GIL; a batch is submitted without blocking
+ * (copy_submit) and waited for later (copy_wait), so the caller can queue the next staging buffer and issue transfers
+ * while the threads copy. */
+#include <immintrin.h>
+#include <stdatomic.h>
+#include <sys/types.h>
+#include <unistd.h>
+
+#define POOL_MAX 16
+#define QUEUE_MAX 16
+#define JOB_BYTES ((size_t)1 << 20)
+
+typedef struct {
+    char *dst;
+    const char *src;      /* memory source, or NULL when the batch reads a file */
+    long long file_off;
+    size_t len;
+} Job;
+
+typedef struct {
+    Job *jobs;
+    size_t njobs, next, unfinished;
+    int fd, failed, done, in_use;
+    unsigned long id;
+} Batch;
+
+static struct {
+    pthread_mutex_t mu;
+    pthread_cond_t work, finished;
+    int nthreads;
+    pid_t owner;
+    Batch q[QUEUE_MAX];
+    unsigned long next_id;
+} pool = {PTHREAD_MUTEX_INITIALIZER, PTHREAD_COND_INITIALIZER, PTHREAD_COND_INITIALIZER};
+
+/* memcpy whose stores bypass the caches. The destination is a page-locked staging buffer that the GPU's copy engine
+ * reads next: with ordinary stores its lines sit dirty in the L2s of a dozen cores and every DMA read has to snoop
+ * them out (64 MB through the ring: 3.8 ms; with streaming stores 1.8 ms), and every store costs a
+ * read-for-ownership (12 threads: 60 -> 75 GB/s). tools/ring_probe.py, SNT_CACHED_STAGING=1 for the A/B. */
+__attribute__((target("avx2"))) static void copy_stream_avx2(char *dst, const char *src, size_t n) {
+    size_t head = (32 - ((uintptr_t)dst & 31)) & 31;
+    if (head > n) head = n;
+    if (head) { memcpy(dst, src, head); dst += head; src += head; n -= head; }
+    size_t i = 0;
+    for (; i + 128 <= n; i += 128) {
+        __m256i a = _mm256_loadu_si256((const __m256i *)(src + i)), b = _mm256_loadu_si256((const __m256i *)(src + i + 32)),
+                c = _mm256_loadu_si256((const __m256i *)(src + i + 64)), d = _mm256_loadu_si256((const __m256i *)(src + i + 96));
+        _mm256_stream_si256((__m256i *)(dst + i), a); _mm256_stream_si256((__m256i *)(dst + i + 32), b);
+        _mm256_stream_si256((__m256i *)(dst + i + 64), c); _mm256_stream_si256((__m256i *)(dst + i + 96), d);
+    }
+    for (; i + 32 <= n; i += 32) _mm256_stream_si256((__m256i *)(dst + i), _mm256_loadu_si256((const __m256i *)(src + i)));
+    if (i < n) memcpy(dst + i, src + i, n - i);
+    _mm_sfence();
+}
+
+static int g_stream_stores = -1;      /* -1: not decided yet */
+
+static void copy_to_staging(char *dst, const char *src, size_t n) {
+    if (g_stream_stores < 0) {
+        const char *e = getenv("SNT_CACHED_STAGING");
+        g_stream_stores = (!e || !*e || *e == '0') && __builtin_cpu_supports("avx2");
+    }
+    if (g_stream_stores && n >= 4096) copy_stream_avx2(dst, src, n);
+    else memcpy(dst, src, n);
+}
+
+static int run_job(const Job *j, int fd) {
+    if (fd < 0) { copy_to_staging(j->dst, j->src, j->len); return 0; }
+    size_t got = 0;
+    while (got < j->len) {
+        ssize_t r = pread(fd, j->dst + got, j->len - got, (off_t)(j->file_off + (long long)got));
+        if (r <= 0) return -1;
+        got += (size_t)r;
+    }
+    return 0;
+}
+
+/* Oldest batch that still has a job to hand out (pool.mu held). */
+static Batch *next_batch(void) {
+    Batch *best = NULL;
+    for (int i = 0; i < QUEUE_MAX; ++i) {
+        Batch *b = &pool.q[i];
+        if (b->in_use && b->next < b->njobs && (!best || b->id < best->id)) best = b;
+    }
+    return best;
+}
+
+static void *pool_worker(void *arg) {
+    (void)arg;
+    pthread_mutex_lock(&pool.mu);
+    for (;;) {
+        Batch *b = next_batch();
+        if (!b) { pthread_cond_wait(&pool.work, &pool.mu); continue; }
+        const Job *j = &b->jobs[b->next++];
+        const int fd = b->fd;
+        pthread_mutex_unlock(&pool.mu);
+        const int rc = run_job(j, fd);
+        pthread_mutex_lock(&pool.mu);
+        if (rc) b->failed = 1;
+        if (--b->unfinished == 0) { b->done = 1; pthread_cond_broadcast(&pool.finished); }
+    }
+    return NULL;
+}
+
+/* Queue a batch (takes ownership of jobs). Returns its id (> 0), or 0 when the queue is full / no thread could be made. */
+static unsigned long pool_submit(Job *jobs, size_t njobs, int fd, int threads) {
+    if (threads > POOL_MAX) threads = POOL_MAX;
+    if (threads < 1) threads = 1;
+    pthread_mutex_lock(&pool.mu);
+    if (pool.owner != getpid()) {                     /* first use, or the child of a fork(): no threads, no batches */
+        pool.owner = getpid(); pool.nthreads = 0;
+        memset(pool.q, 0, sizeof pool.q);
+    }
+    while (pool.nthreads < threads) {
+        pthread_t t;
+        if (pthread_create(&t, NULL, pool_worker, NULL) != 0) break;
+        pthread_detach(t);
+        ++pool.nthreads;
+    }
+    Batch *b = NULL;
+    for (int i = 0; i < QUEUE_MAX && !b; ++i) if (!pool.q[i].in_use) b = &pool.q[i];
+    if (!b || pool.nthreads == 0) { pthread_mutex_unlock(&pool.mu); return 0; }
+    b->jobs = jobs; b->njobs = njobs; b->next = 0; b->unfinished = njobs; b->fd = fd;
+    b->failed = 0; b->done = njobs == 0; b->in_use = 1; b->id = ++pool.next_id;
+    const unsigned long id = b->id;
+    pthread_cond_broadcast(&pool.work);
+    pthread_mutex_unlock(&pool.mu);
+    return id;
+}
+
+/* Wait for a batch and release it. 0 = copied, -1 = short read, -2 = unknown id. GIL must be released. */
+static int pool_wait(unsigned long id) {
+    pthread_mutex_lock(&pool.mu);
+    Batch *b = NULL;
+    for (int i = 0; i < QUEUE_MAX; ++i) if (pool.q[i].in_use && pool.q[i].id == id) b = &pool.q[i];
+    if (!b) { pthread_mutex_unlock(&pool.mu); return -2; }
+    while (!b->done) pthread_cond_wait(&pool.finished, &pool.mu);
+    const int rc = b->failed ? -1 : 0;
+    Job *jobs = b->jobs;
+    b->in_use = 0; b->jobs = NULL;
+    pthread_mutex_unlock(&pool.mu);
+    free(jobs);
+    return rc;
+}
+
+/* pieces: flat sequence of ints  dst_addr, src, len, ...  -> malloc'ed 1 MB jobs */
+static Job *parse_pieces(PyObject *seq_in, int fd, size_t *njobs_out, size_t *total_out) {
+    PyObject *seq = PySequence_Fast(seq_in, "expected a flat sequence of integers");
+    if (!seq) return NULL;
+    size_t n = (size_t)PySequence_Fast_GET_SIZE(seq);
+    PyObject **items = PySequence_Fast_ITEMS(seq);
+    if (n % 3) { Py_DECREF(seq); PyErr_SetString(PyExc_ValueError, "pieces come in (dst, src, len) triples"); return NULL; }
+    size_t njobs = 0, total = 0;
+    for (size_t i = 0; i < n; i += 3) {
+        unsigned long long len = PyLong_AsUnsignedLongLong(items[i + 2]);
+        if (len == (unsigned long long)-1 && PyErr_Occurred()) { Py_DECREF(seq); return NULL; }
+        njobs += (size_t)((len + JOB_BYTES - 1) / JOB_BYTES);
+        total += (size_t)len;
+    }
+    Job *jobs = (Job *)malloc((njobs ? njobs : 1) * sizeof(Job));
+    if (!jobs) { Py_DECREF(seq); PyErr_NoMemory(); return NULL; }
+    size_t k = 0;
+    for (size_t i = 0; i < n; i += 3) {
+        unsigned long long dst = PyLong_AsUnsignedLongLong(items[i]), src = PyLong_AsUnsignedLongLong(items[i + 1]),
+                           len = PyLong_AsUnsignedLongLong(items[i + 2]);
+        if (PyErr_Occurred()) { free(jobs); Py_DECREF(seq); return NULL; }
+        for (unsigned long long o = 0; o < len; o += JOB_BYTES) {
+            jobs[k].dst = (char *)(uintptr_t)(dst + o);
+            jobs[k].src = fd < 0 ? (const char *)(uintptr_t)(src + o) : NULL;
+            jobs[k].file_off = (long long)(src + o);
+            jobs[k].len = (size_t)(len - o < JOB_BYTES ? len - o : JOB_BYTES);
+            ++k;
+        }
+    }
+    Py_DECREF(seq);
+    *njobs_out = njobs; *total_out = total;
+    return jobs;
+}
+
+/* copy_submit(pieces, fd=-1, threads=12) -> batch id (0: nothing to copy). The memory the pieces name (and the
+ * file) must stay valid until copy_wait(id) returns. */
+static PyObject *hp_copy_submit(PyObject *self, PyObject *args) {
+    PyObject *seq_in;
+    int fd = -1, threads = 12;
+    if (!PyArg_ParseTuple(args, "O|ii", &seq_in, &fd, &threads)) return NULL;
+    size_t njobs = 0, total = 0;
+    Job *jobs = parse_pieces(seq_in, fd, &njobs, &total);
+    if (!jobs) return NULL;
+    if (njobs == 0) { free(jobs); return PyLong_FromLong(0); }
+    unsigned long id = pool_submit(jobs, njobs, fd, threads);
+    if (id == 0) {                                    /* queue full or no threads: copy here and now */
+        int rc = 0;
+        Py_BEGIN_ALLOW_THREADS
+        for (size_t i = 0; i < njobs; ++i) rc |= run_job(&jobs[i], fd);
+        Py_END_ALLOW_THREADS
+        free(jobs);
+        if (rc) { PyErr_SetString(PyExc_OSError, "short read while staging a file"); return NULL; }
+        return PyLong_FromLong(0);
+    }
+    return PyLong_FromUnsignedLong(id);
+}
+
+/* copy_wait(id): returns when the batch has been copied; OSError on a short read. id 0 is a no-op. */
+static PyObject *hp_copy_wait(PyObject *self, PyObject *args) {
+    unsigned long id;
+    if (!PyArg_ParseTuple(args, "k", &id)) return NULL;
+    if (id == 0) Py_RETURN_NONE;
+    int rc;
+    Py_BEGIN_ALLOW_THREADS
+    rc = pool_wait(id);
+    Py_END_ALLOW_THREADS
+    if (rc == -1) { PyErr_SetString(PyExc_OSError, "short read while staging a file"); return NULL; }
+    if (rc == -2) { PyErr_SetString(PyExc_ValueError, "unknown copy batch"); return NULL; }
+    Py_RETURN_NONE;
+}
+
+/* copy_many(pieces, fd=-1, threads=12) -> bytes copied: copy_submit + copy_wait. */
+static PyObject *hp_copy_many(PyObject *self, PyObject *args) {
+    PyObject *seq_in;
+    int fd = -1, threads = 12;
+    if (!PyArg_ParseTuple(args, "O|ii", &seq_in, &fd, &threads)) return NULL;
+    size_t njobs = 0, total = 0;
+    Job *jobs = parse_pieces(seq_in, fd, &njobs, &total);
+    if (!jobs) return NULL;
+    int rc = 0;
+    if (njobs) {
+        Py_BEGIN_ALLOW_THREADS
+        unsigned long id = pool_submit(jobs, njobs, fd, threads);
+        if (id) rc = pool_wait(id);
+        else { for (size_t i = 0; i < njobs; ++i) rc |= run_job(&jobs[i], fd); free(jobs); }
+        Py_END_ALLOW_THREADS
+    } else {
+        free(jobs);
+    }
+    if (rc != 0) { PyErr_SetString(PyExc_OSError, "short read while staging a file"); return NULL; }
+    return PyLong_FromSize_t(total);
+}
+
 static PyMethodDef methods[] = {
+    {"copy_many", hp_copy_many, METH_VARARGS, "copy_many(pieces, fd=-1, threads=12) -> bytes copied"},
+    {"copy_submit", hp_copy_submit, METH_VARARGS, "copy_submit(pieces, fd=-1, threads=12) -> batch id"},
+    {"copy_wait", hp_copy_wait, METH_VARARGS, "copy_wait(batch id)"},
     {"manifest_columns", hp_manifest_columns, METH_VARARGS,
      "manifest_columns(rows, ids_addr, src_addr, off_addr, len_addr) -> (code, index)"},
     {"gather", hp_gather, METH_VARARGS, "gather(seq, dst_addr, capacity, lens_addr, threads=8) -> total bytes"},

@@ -182,14 +182,24 @@ class StagingRing:
 def staging_threads(workers: int = 1) -> int:
     import os
 
-    # 12 copy threads on a 16-core box: tools/hostcopy_probe.py measures 48 / 54 / 59 GB/s for 8 / 12 / 16 threads;
-    # the calling thread and the driver need cores too
+    # Python pool (no helper): 12 copy threads on a 16-core box -- tools/hostcopy_probe.py measures 48 / 54 / 59 GB/s for
+    # 8 / 12 / 16 threads. C pool with streaming stores: 8 threads already copy 74 GB/s (tools/ring_probe.py), more only
+    # compete with the copy engine for memory bandwidth (GPT2-XL from pageable memory: 139 / 136 / 133 / 139 / 141 ms with
+    # 6 / 8 / 10 / 12 / 16 threads); the calling thread and the driver need cores too
     cpus = os.cpu_count() or 1
-    return max(1, min(16, max(int(workers), min(12, max(1, cpus - 4)))))
+    forced = os.environ.get("SNT_STAGE_THREADS")           # probes only (tools/host_small_probe.py)
+    if forced:
+        return max(1, min(16, int(forced)))
+    return max(1, min(16, max(int(workers), min(10 if _hostpack is not None else 12, max(1, cpus - 4)))))
 
 
 STAGE_DIRECT_MAX_BYTES = 8 << 20       # smaller pageable buffers take the plain (synchronous) copy
 STAGE_INLINE_MAX_BYTES = 256 << 10     # pieces below this are copied by the calling thread, not the pool
+
+
+import os as _os
+
+_copy_pool = _hostpack if not _os.environ.get("SNT_NO_COPY_POOL") else None      # A/B switch for tools/host_small_probe.py
 
 
 class RingWriter:
@@ -200,6 +210,10 @@ class RingWriter:
     tasks have finished -- up to ``MAX_PENDING`` closed buffers wait like that while the caller already queues
     the tasks of the next one, so the pool never drains while the caller waits (the first version waited for
     every buffer before touching the next: 23-30 GB/s from pageable memory on a box whose threads copy 54 GB/s).
+    With the C helper the copy threads live in C (``_hostpack.copy_submit`` / ``copy_wait``: 1 MB jobs, no GIL, no
+    task objects, **streaming stores** -- the copy engine reads the staging buffer next, and lines left dirty in a
+    dozen L2 caches by ordinary stores have to be snooped out by every DMA read: 64 MB through the ring 3.8 -> 1.8 ms,
+    a GPT-2-small-sized state dict 19.3 -> 15.5 ms); the Python pool is the path without the helper.
     The caller must hold ``ring.lock``.
     """
 
@@ -208,18 +222,32 @@ class RingWriter:
         self.MAX_PENDING = max(0, min(2, len(ring.bufs) - 2))   # the slot being acquired is never one that still waits
         self.slot, self.base, self.fill, self.tasks = -1, 0, 0, []
         self.pending: "collections.deque" = collections.deque()
+        self.fd = -1                         # >= 0: the pieces of this writer are file offsets (write_file)
+        self.keep: list = []                 # source arrays of the pieces not copied yet
 
     def write(self, off: int, src: np.ndarray) -> None:
         """Queue the copy of flat uint8 ``src`` to ``dst[off : off + len(src)]``."""
-        self._write(off, int(src.shape[0]), lambda view, p0, p1: np.copyto(view, src[p0:p1]))
+        if _copy_pool is not None:
+            self.keep.append(src)
+            self._write(off, int(src.shape[0]), None, src.__array_interface__["data"][0])
+        else:
+            self._write(off, int(src.shape[0]), lambda view, p0, p1: np.copyto(view, src[p0:p1]), 0)
 
     def write_file(self, off: int, fd: int, file_off: int, n: int) -> None:
         """Queue ``n`` bytes of the open file ``fd`` from ``file_off`` to ``dst[off : off + n]``: the staging threads
-        ``pread`` straight into the pinned buffers (one copy out of the page cache, none through a ``bytes`` object)."""
-        self._write(off, n, lambda view, p0, p1: _pread_exact(fd, view, file_off + p0))
+        ``pread`` straight into the pinned buffers (one copy out of the page cache, none through a ``bytes`` object).
+        One writer reads from one file."""
+        if _copy_pool is not None:
+            self.fd = fd
+            self._write(off, n, None, file_off)
+        else:
+            self._write(off, n, lambda view, p0, p1: _pread_exact(fd, view, file_off + p0), 0)
 
-    def _write(self, off: int, n: int, copy) -> None:
-        """``copy(view, p0, p1)`` fills the pinned ``view`` with source bytes [p0, p1); it runs on the pool for large pieces."""
+    def _write(self, off: int, n: int, copy, src_base: int) -> None:
+        """With the C helper the pieces ``(pinned address, source address or file offset, length)`` of a staging
+        buffer are collected and copied by its thread pool when the buffer is closed (``copy_many``: no GIL, no
+        task objects). Without it ``copy(view, p0, p1)`` fills the pinned ``view`` with source bytes [p0, p1) on the
+        Python pool for large pieces."""
         pos = 0
         ring = self.ring
         while pos < n:
@@ -233,7 +261,9 @@ class RingWriter:
             view = ring.views[self.slot]
             if so > self.fill:
                 view[self.fill:so] = 0                      # alignment gap between two buffers: defined bytes
-            if take < STAGE_INLINE_MAX_BYTES:               # a task costs more than a small memcpy
+            if copy is None:
+                self.tasks += (ring.bufs[self.slot].data_ptr() + so, src_base + pos, take)
+            elif take < STAGE_INLINE_MAX_BYTES:             # a task costs more than a small memcpy
                 copy(view[so:so + take], pos, pos + take)
             else:
                 for p0 in range(0, take, STAGE_PIECE_BYTES):
@@ -247,7 +277,14 @@ class RingWriter:
     def close(self) -> None:
         """End the current staging buffer (the next write starts a new one, at any destination offset)."""
         if self.slot >= 0 and self.fill:
-            self.pending.append((self.slot, self.base, self.fill, self.tasks))
+            if _copy_pool is not None:
+                # the C pool starts filling the buffer now; the transfer is issued when a later buffer is closed (or at
+                # drain), so the threads copy while the caller queues more and the copy engine moves the older buffers
+                handle = _copy_pool.copy_submit(self.tasks, self.fd, self.ring.threads)
+                self.pending.append((self.slot, self.base, self.fill, (handle, self.keep)))
+                self.keep = []
+            else:
+                self.pending.append((self.slot, self.base, self.fill, self.tasks))
             while len(self.pending) > self.MAX_PENDING:
                 self._issue(self.pending.popleft())
         elif self.slot >= 0:
@@ -256,13 +293,33 @@ class RingWriter:
 
     def _issue(self, item) -> None:
         slot, base, fill, tasks = item
-        for t in tasks:
-            t.result()
+        if isinstance(tasks, tuple):
+            _copy_pool.copy_wait(tasks[0])                  # (handle, source arrays kept alive until here)
+        else:
+            for t in tasks:
+                t.result()
         with torch.cuda.stream(self.stream):
             self.dst[base:base + fill].copy_(self.ring.bufs[slot][:fill], non_blocking=True)
             ev = torch.cuda.Event()
             ev.record(self.stream)
         self.ring.events[slot] = ev
+
+    def abandon(self) -> None:
+        """Wait for every copy still queued without issuing its transfer (error paths: the sources are about to go away)."""
+        while self.pending:
+            tasks = self.pending.popleft()[3]
+            try:
+                if isinstance(tasks, tuple):
+                    _copy_pool.copy_wait(tasks[0])
+                else:
+                    for t in tasks:
+                        t.exception()
+            except OSError:
+                pass
+        for t in self.tasks:
+            if hasattr(t, "exception"):
+                t.exception()
+        self.slot, self.fill, self.tasks, self.keep = -1, 0, [], []
 
     def drain(self) -> None:
         """Issue every transfer queued so far (they are then ordered on ``stream``)."""
@@ -281,9 +338,12 @@ def pageable_to_device(src: np.ndarray, dst: torch.Tensor, workers: int = 1) -> 
     stream = torch.cuda.current_stream()
     with ring.lock:
         w = RingWriter(ring, dst, stream)
-        w.write(0, src)
-        w.drain()
-        stream.synchronize()      # the ring may be handed to another caller / stream after the lock is released
+        try:
+            w.write(0, src)
+            w.drain()
+        finally:
+            w.abandon()
+            stream.synchronize()  # the ring may be handed to another caller / stream after the lock is released
 
 
 def _pread_exact(fd: int, view: np.ndarray, file_off: int) -> None:
@@ -317,9 +377,7 @@ def file_to_device(path, device: Optional[torch.device] = None, workers: int = 1
                 w.write_file(0, f.fileno(), 0, size)
                 w.drain()
             finally:
-                for item in list(w.pending) + [(0, 0, 0, w.tasks)]:      # no task may outlive the file descriptor
-                    for t in item[3]:
-                        t.exception()
+                w.abandon()                                              # no copy may outlive the file descriptor
                 stream.synchronize()
     return out
 
@@ -351,10 +409,13 @@ def pageable_arena(arrays: Sequence[np.ndarray], device: torch.device, workers: 
     stream = torch.cuda.current_stream()
     with ring.lock:
         w = RingWriter(ring, arena, stream)
-        for a, off in zip(arrays, offs):
-            w.write(off, a)
-        w.drain()
-        stream.synchronize()          # the ring goes back to the pool only when no transfer still reads it
+        try:
+            for a, off in zip(arrays, offs):
+                w.write(off, a)
+            w.drain()
+        finally:
+            w.abandon()
+            stream.synchronize()      # the ring goes back to the pool only when no transfer still reads it
     return arena, offs
 
 

@@ -351,6 +351,7 @@ def _inplace_merkle_host(cfg: HashConfig, model: TensorMap, workers: int = 1) ->
     if staging is not None:
         staging.lock.acquire()                             # one staged hash at a time owns the pinned staging ring
     plan = None
+    writer = None
     try:
         writer = _dev.RingWriter(staging, ring, side) if staging is not None else None
         copied: List[Optional[torch.cuda.Event]] = [None] * len(groups)
@@ -427,6 +428,8 @@ def _inplace_merkle_host(cfg: HashConfig, model: TensorMap, workers: int = 1) ->
         return ModelDigestResult(root, cfg, n_leaves, aux_digest_bytes=aux)
     finally:
         # no copy may still be in flight when the ring goes back to the allocator or the staging ring to its next owner
+        if writer is not None:
+            writer.abandon()                                # (a no-op unless an exception left staged copies behind)
         torch.cuda.synchronize()
         if staging is not None:
             staging.lock.release()

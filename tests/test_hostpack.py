@@ -112,3 +112,33 @@ def test_manifest_columns():
     assert _hostpack.manifest_columns([(1, 1, b"", 1 << 70, 1)], *ptrs) == (5, 0)      # caller's Python path decides
     assert _hostpack.manifest_columns([[1, 1, b"", 0, 1]], *ptrs) == (5, 0)            # not a tuple
     assert _hostpack.manifest_columns([], *ptrs) == (0, 0)
+
+
+def test_copy_many_memory_and_file(tmp_path):
+    rng = np.random.default_rng(4)
+    src = rng.integers(0, 256, size=(9 << 20) + 123, dtype=np.uint8)
+    dst = np.zeros(src.size + 64, dtype=np.uint8)
+    pieces = []
+    for o in range(0, src.size, (2 << 20) + 77):                      # pieces at odd offsets, cut into 1 MB jobs inside
+        ln = min((2 << 20) + 77, src.size - o)
+        pieces += [dst.ctypes.data + 32 + o, src.ctypes.data + o, ln]
+    for threads in (1, 3, 12):
+        dst[:] = 0
+        assert _hostpack.copy_many(pieces, -1, threads) == src.size
+        assert np.array_equal(dst[32:32 + src.size], src) and not dst[:32].any() and not dst[32 + src.size:].any()
+    path = tmp_path / "shard.bin"
+    path.write_bytes(src.tobytes())
+    import os
+
+    fd = os.open(path, os.O_RDONLY)
+    try:
+        dst[:] = 0
+        assert _hostpack.copy_many([dst.ctypes.data, 7, src.size - 7], fd, 4) == src.size - 7
+        assert np.array_equal(dst[:src.size - 7], src[7:])
+        with pytest.raises(OSError):
+            _hostpack.copy_many([dst.ctypes.data, src.size - 10, 100], fd, 2)     # runs past the end of the file
+    finally:
+        os.close(fd)
+    assert _hostpack.copy_many([]) == 0
+    with pytest.raises(ValueError):
+        _hostpack.copy_many([1, 2])
