@@ -77,8 +77,12 @@ def build_hostpack(force: bool = False) -> Path:
     src = CSRC / "hostpack.c"
     if not force and _newer(HOSTPACK_LIB, [src]):
         return HOSTPACK_LIB
-    _run(["gcc", "-O2", "-std=c11", "-fPIC", "-shared", "-pthread", "-Wall",
-          "-I" + sysconfig.get_paths()["include"], src, "-o", HOSTPACK_LIB])
+    try:
+        _run(["gcc", "-O2", "-std=gnu11", "-fPIC", "-shared", "-pthread", "-Wall",
+              "-I" + sysconfig.get_paths()["include"], src, "-o", HOSTPACK_LIB])
+    except RuntimeError as exc:
+        # the package runs without the helper (Python packers, same bytes); say so instead of failing the build
+        sys.stderr.write(f"warning: _hostpack.so not built ({exc}); the reference-shaped calls pack in Python\n")
     return HOSTPACK_LIB
 
 
