@@ -357,6 +357,21 @@ def _pread_exact(fd: int, view: np.ndarray, file_off: int) -> None:
         got += r
 
 
+def read_file_host(path, workers: int = 1) -> np.ndarray:
+    """The bytes of a file as one uint8 array in (pageable) host memory. Large files are read by the C pool's
+    threads in parallel (``pread`` of 1 MB jobs straight into the array, whose pages the threads also fault in):
+    ``Path.read_bytes`` moves 2.5 GB/s on one thread. Raises ``OSError`` like ``open``/``read``."""
+    import os
+
+    with open(path, "rb", buffering=0) as f:
+        size = os.fstat(f.fileno()).st_size
+        if _hostpack is None or size < STAGE_DIRECT_MAX_BYTES:
+            return np.frombuffer(f.read(), dtype=np.uint8)
+        out = np.empty(size, dtype=np.uint8)
+        _hostpack.copy_many([out.ctypes.data, 0, size], f.fileno(), staging_threads(workers))
+    return out
+
+
 def file_to_device(path, device: Optional[torch.device] = None, workers: int = 1) -> torch.Tensor:
     """The bytes of a file as a flat uint8 CUDA tensor. Large files are read by the staging threads straight into
     the pinned ring and transferred buffer by buffer while the next one is being read (``read_bytes`` + copy of a

@@ -723,13 +723,15 @@ def load_model(manifest_path) -> TensorMap:
     manifest_path = Path(manifest_path)
     try:
         doc = json.loads(manifest_path.read_text())
-        raw = (manifest_path.parent / doc["data"]).read_bytes()
+        # one parallel read of the data file; every tensor is a read-only view of it (compares equal to the ``bytes``
+        # the reference builds, model.py:335-352, without a second copy of the checkpoint)
+        raw = memoryview(_dev.read_file_host(manifest_path.parent / doc["data"])).toreadonly()
         entries = []
         for rec in doc["tensors"]:
             start, length = int(rec["offset"]), int(rec["length"])
             if start < 0 or length < 0 or start + length > len(raw):
                 raise FormatError(f"tensor {rec['name']!r} range [{start}, {start + length}) exceeds data file")
-            entries.append((rec["name"], bytes(raw[start:start + length])))
+            entries.append((rec["name"], raw[start:start + length]))
     except FormatError:
         raise
     except (OSError, KeyError, ValueError, TypeError) as exc:

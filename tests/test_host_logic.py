@@ -128,6 +128,20 @@ def test_model_manifest_round_trip(tmp_path):
         pkg.load_model(tmp_path / "r.json")
 
 
+def test_model_manifest_large_file_is_read_in_parallel_and_viewed(tmp_path):
+    """A data file above the direct-read threshold goes through the C pool (parallel pread); every tensor is a
+    read-only view that still compares equal to the ``bytes`` the reference builds (model.py:335-352)."""
+    rng = random.Random(44)
+    sizes = [5 << 20, 0, 3, (4 << 20) + 17, 8192]
+    tm = pkg.TensorMap([(f"l{i}", rng.randbytes(n)) for i, n in enumerate(sizes)])
+    pkg.save_model(tm, tmp_path / "big.json")
+    loaded = pkg.load_model(tmp_path / "big.json")
+    assert loaded.entries == tm.entries and loaded.total_bytes == sum(sizes)
+    assert all(memoryview(buf).readonly for _, buf in loaded.entries)
+    pkg.save_model(loaded, tmp_path / "again.json")
+    assert (tmp_path / "again.bin").read_bytes() == (tmp_path / "big.bin").read_bytes()
+
+
 def test_dataset_manifest_round_trip_and_validation(tmp_path):
     samples = inputs.dataset_samples(**inputs.DATASET_CASES[0])
     shard, off, ln, ids, src = inputs.pack_samples(samples)
