@@ -228,6 +228,9 @@ class RingWriter:
     def write(self, off: int, src: np.ndarray) -> None:
         """Queue the copy of flat uint8 ``src`` to ``dst[off : off + len(src)]``."""
         if _copy_pool is not None:
+            if self.fd != -1 and self.tasks:
+                self.close()                                # a batch of the C pool reads memory OR one file
+            self.fd = -1
             self.keep.append(src)
             self._write(off, int(src.shape[0]), None, src.__array_interface__["data"][0])
         else:
@@ -236,8 +239,10 @@ class RingWriter:
     def write_file(self, off: int, fd: int, file_off: int, n: int) -> None:
         """Queue ``n`` bytes of the open file ``fd`` from ``file_off`` to ``dst[off : off + n]``: the staging threads
         ``pread`` straight into the pinned buffers (one copy out of the page cache, none through a ``bytes`` object).
-        One writer reads from one file."""
+        """
         if _copy_pool is not None:
+            if self.fd != fd and self.tasks:
+                self.close()
             self.fd = fd
             self._write(off, n, None, file_off)
         else:

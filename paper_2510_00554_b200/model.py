@@ -51,7 +51,76 @@ class Strategy(enum.Enum):
     IN_PLACE = "in-place"
 
 
+class _OpenFile:
+    """A data file kept open for the tensors that view it (closed when the last of them is gone)."""
+
+    def __init__(self, path):
+        import os
+
+        self.path = path
+        self.fd = os.open(path, os.O_RDONLY)
+        self.size = os.fstat(self.fd).st_size
+        self._whole: Optional[memoryview] = None
+
+    def whole(self) -> memoryview:
+        """The file's bytes in host memory, read ONCE (in parallel, ``device.read_file_host``) when a consumer other
+        than the in-place GPU path first asks for any tensor's bytes."""
+        if self._whole is None:
+            self._whole = memoryview(_dev.read_file_host(self.path)).toreadonly()
+            if len(self._whole) < self.size:
+                raise FormatError(f"data file {self.path} shrank while it was open")
+        return self._whole
+
+    def __del__(self, _close=__import__("os").close):      # (bound now: at interpreter shutdown imports no longer work)
+        try:
+            _close(self.fd)
+        except OSError:
+            pass
+
+
+class FileTensor:
+    """Bytes [offset, offset + nbytes) of a checkpoint's data file, read only when somebody needs them.
+
+    ``load_model`` hands these out: ``hash_model`` on the in-place path has the staging threads ``pread`` each
+    piece straight into the pinned ring (file -> page-locked memory -> HBM, no copy of the checkpoint in host
+    memory at all). Everything else sees an ordinary read-only bytes-like object: it exports the buffer protocol
+    (PEP 688; the first use reads the whole file once, in parallel, and every tensor is then a view of that) and
+    compares equal to the ``bytes`` the reference builds (model.py:335-352).
+    """
+
+    __slots__ = ("file", "offset", "nbytes")
+    __hash__ = None
+
+    def __init__(self, file: _OpenFile, offset: int, nbytes: int):
+        self.file, self.offset, self.nbytes = file, offset, nbytes
+
+    def view(self) -> memoryview:
+        return self.file.whole()[self.offset:self.offset + self.nbytes]
+
+    def __buffer__(self, flags):                            # np.frombuffer / memoryview / bytes() all work
+        return self.view()
+
+    def tobytes(self) -> bytes:
+        return bytes(self.view())
+
+    __bytes__ = tobytes
+
+    def __len__(self) -> int:
+        return self.nbytes
+
+    def __eq__(self, other):
+        try:
+            return self.view() == memoryview(other)
+        except TypeError:
+            return NotImplemented
+
+    def __repr__(self) -> str:
+        return f"FileTensor(offset={self.offset}, nbytes={self.nbytes})"
+
+
 def buffer_nbytes(buf) -> int:
+    if isinstance(buf, FileTensor):
+        return buf.nbytes
     if isinstance(buf, torch.Tensor):
         return buf.numel() * buf.element_size()
     if isinstance(buf, np.ndarray):
@@ -265,7 +334,7 @@ def _inplace_merkle_host(cfg: HashConfig, model: TensorMap, workers: int = 1) ->
     lib = _dev._native.load()
     bs = cfg.block_size
     entries = model.entries
-    CUDA, PINNED, PAGEABLE, SMALL = 0, 1, 2, 3
+    CUDA, PINNED, PAGEABLE, SMALL, FILE = 0, 1, 2, 3, 4
     piece = max(bs, STAGE_PIECE_BYTES // bs * bs)
     small_limit = SMALL_H2D_BYTES if lib.snt_device_reads_pinned_host() else 0
 
@@ -282,6 +351,10 @@ def _inplace_merkle_host(cfg: HashConfig, model: TensorMap, workers: int = 1) ->
             t = _dev.as_device_bytes(buf, dev)
             keep.append(t)
             spans.append((CUDA, t, 0, nbytes))
+        elif isinstance(buf, FileTensor):
+            keep.append(buf)                               # pread by the staging threads straight into the pinned ring
+            spans.extend((FILE, buf, o, min(piece, nbytes - o)) for o in range(0, nbytes, piece))
+            n_pageable += 1
         elif is_tensor and buf.is_pinned() and buf.is_contiguous():
             if nbytes < small_limit:
                 spans.append((SMALL, buf, 0, nbytes))
@@ -300,7 +373,7 @@ def _inplace_merkle_host(cfg: HashConfig, model: TensorMap, workers: int = 1) ->
     def aligned(x: int) -> int:
         return -(-x // _ARENA_ALIGN) * _ARENA_ALIGN
 
-    ring_need = sum(aligned(sp[3]) for sp in spans if sp[0] in (PINNED, PAGEABLE))
+    ring_need = sum(aligned(sp[3]) for sp in spans if sp[0] in (PINNED, PAGEABLE, FILE))
     ring_bytes = min(ring_need, (STAGE_RING_GROUPS + 1) * (STAGE_CHUNK_BYTES + aligned(piece)))
     small_bytes = sum(aligned(sp[3]) for sp in spans if sp[0] == SMALL)
     ring = torch.empty(max(ring_bytes, 16), dtype=torch.uint8, device=dev)
@@ -383,6 +456,9 @@ def _inplace_merkle_host(cfg: HashConfig, model: TensorMap, workers: int = 1) ->
                 elif kind == PAGEABLE:
                     flush_pinned()
                     writer.write(offs[i], src[off:off + nbytes])
+                elif kind == FILE:
+                    flush_pinned()
+                    writer.write_file(offs[i], src.file.fd, src.offset + off, nbytes)
             if writer is not None:
                 writer.drain()
             flush_pinned()
@@ -723,15 +799,14 @@ def load_model(manifest_path) -> TensorMap:
     manifest_path = Path(manifest_path)
     try:
         doc = json.loads(manifest_path.read_text())
-        # one parallel read of the data file; every tensor is a read-only view of it (compares equal to the ``bytes``
-        # the reference builds, model.py:335-352, without a second copy of the checkpoint)
-        raw = memoryview(_dev.read_file_host(manifest_path.parent / doc["data"])).toreadonly()
+        # the data file stays open; every tensor is a lazy read-only view of its byte range (see FileTensor)
+        data = _OpenFile(manifest_path.parent / doc["data"])
         entries = []
         for rec in doc["tensors"]:
             start, length = int(rec["offset"]), int(rec["length"])
-            if start < 0 or length < 0 or start + length > len(raw):
+            if start < 0 or length < 0 or start + length > data.size:
                 raise FormatError(f"tensor {rec['name']!r} range [{start}, {start + length}) exceeds data file")
-            entries.append((rec["name"], raw[start:start + length]))
+            entries.append((rec["name"], FileTensor(data, start, length)))
     except FormatError:
         raise
     except (OSError, KeyError, ValueError, TypeError) as exc:

@@ -928,3 +928,39 @@ def test_process_batch_helper_and_python_packer_agree(pkg):
                 pkg.process_batch(pkg.Batch([pkg.SampleRecord(1 << 64, 1, b"", b"x")]), acc)
     finally:
         dev._hostpack = helper
+
+
+def test_loaded_checkpoint_file_hashes_like_its_bytes(pkg, porc, tmp_path):
+    """load_model hands out lazy views of the data file (FileTensor): the in-place path preads them straight into
+    the pinned ring, every other strategy reads the file once; all seven configurations must equal the hash of the
+    same tensors held as bytes, and the in-place Merkle root the oracle's (model.py:298-315, :335-352)."""
+    import random
+
+    rng = random.Random(77)
+    sizes = [100, 8192, 0, 5000, (29 << 20) + 13, 3, 40 * 8192, (5 << 20)]      # above the pipelined path's threshold
+    host = [rng.randbytes(s) for s in sizes]
+    tm = pkg.TensorMap([(f"t{i}", h) for i, h in enumerate(host)])
+    pkg.save_model(tm, tmp_path / "ckpt.json")
+    C, S, A = pkg.Construction, pkg.Strategy, pkg.CompressionAlg
+    for cons, strat, alg, ordered in [(C.MERKLE, S.IN_PLACE, A.SHA256, False), (C.MERKLE, S.IN_PLACE, A.SHA3_256, False),
+                                      (C.MERKLE, S.PER_LAYER, A.BLAKE2B, False), (C.MERKLE, S.COALESCED, A.SHA256, False),
+                                      (C.LATTICE, S.IN_PLACE, A.BLAKE2B, False), (C.LATTICE, S.PER_LAYER, A.BLAKE2B, True),
+                                      (C.LATTICE, S.COALESCED, A.BLAKE2B, False)]:
+        cfg = pkg.HashConfig(cons, strat, alg, 8192, ordered)
+        loaded = pkg.load_model(tmp_path / "ckpt.json")          # fresh: nothing materialised yet
+        got, want = pkg.hash_model(cfg, loaded), pkg.hash_model(cfg, tm)
+        assert got.model_digest.data == want.model_digest.data, (cons, strat, alg)
+        assert got.block_count == want.block_count
+        if want.layer_digests is not None:
+            assert {k: d.data for k, d in got.layer_digests.items()} == {k: d.data for k, d in want.layer_digests.items()}
+        if cons is C.MERKLE and strat is S.IN_PLACE:
+            assert got.model_digest.data == porc.inplace_merkle(alg.value, host, 8192)
+            assert loaded.entries[4][1].file._whole is None      # the file was never copied into host memory
+    # a file-backed tensor mixed with bytes, a numpy array and a CUDA tensor in one model
+    import torch
+
+    loaded = pkg.load_model(tmp_path / "ckpt.json")
+    mixed = pkg.TensorMap([("a", loaded.entries[4][1]), ("b", host[1]), ("c", np.frombuffer(host[6], dtype=np.uint8)),
+                           ("d", torch.frombuffer(bytearray(host[7]), dtype=torch.uint8).cuda()), ("e", loaded.entries[3][1])])
+    cfg = pkg.HashConfig(C.MERKLE, S.IN_PLACE, A.SHA256, 8192)
+    assert pkg.hash_model(cfg, mixed).model_digest.data == porc.inplace_merkle("sha256", [host[4], host[1], host[6], host[7], host[3]], 8192)
