@@ -194,3 +194,86 @@ def test_random_models_per_layer_and_coalesced_against_the_python_oracle(pkg, po
         assert pkg.hash_model(m_cfg(pkg.Strategy.COALESCED), model).model_digest.data == porc.coalesced_merkle(alg, host, bs), what
         assert pkg.hash_model(l_cfg(pkg.Strategy.COALESCED), model).model_digest.data == porc.coalesced_lattice(host, bs), what
     print(f"{case} random models x 4 strategy/construction pairs")
+
+
+def test_random_host_object_calls_against_the_python_oracle(pkg, porc, tmp_path):
+    """The reference-shaped calls on Python objects and files (session 4: C packers, file -> pinned ring, lazy
+    checkpoint views): hash_blocks on mixed bytes-like blocks, process_batch on random batches, digest_dataset on
+    a manifest + shard file, load_model + hash_model on a checkpoint file -- against the hashlib oracle."""
+    deadline = time.monotonic() + BUDGET
+    seed0 = int(os.environ.get("SNT_FUZZ_SEED", "13000"))
+    case = 0
+    C, S = pkg.Construction, pkg.Strategy
+    while time.monotonic() < deadline or case < 3:
+        seed = seed0 + case
+        case += 1
+        rng = np.random.default_rng(seed)
+
+        def blob(n):
+            return rng.integers(0, 256, size=int(n), dtype=np.uint8).tobytes()
+
+        def dressed(b):                                   # the same bytes as another bytes-like type
+            k = int(rng.integers(0, 4))
+            return b if k == 0 else bytearray(b) if k == 1 else memoryview(b) if k == 2 else np.frombuffer(b, dtype=np.uint8)
+
+        # ---- hash_blocks + merkle_root over a list of blocks (total below or above the threaded / streaming threshold)
+        alg = ALGS[int(rng.integers(0, 3))]
+        n_blocks = int(rng.choice([1, 2, 9, 300, 1500]))
+        big = int(rng.choice([700, 9000]))
+        blocks = [blob(rng.integers(0, big)) for _ in range(n_blocks)]
+        leaves = pkg.hash_blocks(pkg.CompressionAlg.from_name(alg), [dressed(b) for b in blocks])
+        assert bytes(leaves.data) == bytes(porc.hash_blocks(alg, blocks)), ("hash_blocks", seed)
+        assert pkg.merkle_root(pkg.CompressionAlg.from_name(alg), leaves).data == \
+            porc.merkle_root(alg, bytes(leaves.data), n_blocks), ("merkle_root", seed)
+
+        # ---- process_batch over random batches, and digest_dataset over the same samples as a manifest + shard file
+        n = int(rng.choice([1, 40, 700, 3000]))
+        n_src = int(rng.choice([1, 5, 40]))
+        cover = bool(rng.integers(0, 2))
+        lens = rng.integers(0, int(rng.choice([40, 700, 4000])), size=n)
+        gaps = rng.integers(0, 5, size=n)
+        offs = np.cumsum(lens + gaps) - lens
+        shard = blob(int(offs[-1] + lens[-1]) + 3)
+        ids = rng.integers(0, 1 << 63, size=n, dtype=np.uint64) * 2 + rng.integers(0, 2, size=n, dtype=np.uint64)
+        src = rng.integers(0, n_src, size=n)
+        labels = [blob(k) for k in rng.integers(0, 9, size=n)]
+        samples = [(int(ids[i]), int(src[i]), labels[i], shard[int(offs[i]):int(offs[i] + lens[i])]) for i in range(n)]
+        want = porc.dataset_digests(samples, cover_labels=cover)
+        acc = pkg.SourceAccumulator(cover_labels=cover)
+        order = rng.permutation(n)
+        bs = int(rng.choice([1, 7, 128, 1000]))
+        for s in range(0, n, bs):
+            recs = [pkg.SampleRecord(samples[i][0], samples[i][1], samples[i][2], dressed(samples[i][3]) if i % 5 == 0 else samples[i][3])
+                    for i in order[s:s + bs]]
+            pkg.process_batch(pkg.Batch(recs), acc)
+        assert {k: (d.data, c) for k, (d, c) in pkg.finalize(acc).items()} == want, ("process_batch", seed, cover)
+        rows = [(samples[i][0], samples[i][1], labels[i], int(offs[i]), int(lens[i])) for i in order]
+        (tmp_path / "shard.bin").write_bytes(shard)
+        man = pkg.DatasetManifest(rows, tmp_path / "shard.bin")
+        got = pkg.digest_dataset(man, cover_labels=cover)
+        assert {k: (d.data, c) for k, (d, c) in got.items()} == want, ("digest_dataset", seed, cover)
+
+        # ---- a checkpoint file through load_model (lazy file views), one random configuration
+        sizes = _random_sizes(rng, int(rng.integers(1, 12)), int(rng.choice([20_000, 6 << 20, 40 << 20])))
+        if sum(sizes) == 0:
+            sizes[0] = 17
+        host = [blob(s) for s in sizes]
+        pkg.save_model(pkg.TensorMap([(f"t{i}", h) for i, h in enumerate(host)]), tmp_path / "ckpt.json")
+        loaded = pkg.load_model(tmp_path / "ckpt.json")
+        pick = int(rng.integers(0, 4))
+        if pick == 0:
+            cfg = pkg.HashConfig(C.MERKLE, S.IN_PLACE, pkg.CompressionAlg.from_name(alg), 8192)
+            assert pkg.hash_model(cfg, loaded).model_digest.data == porc.inplace_merkle(alg, host, 8192), ("ckpt merkle", seed)
+        elif pick == 1:
+            cfg = pkg.HashConfig(C.LATTICE, S.IN_PLACE, pkg.CompressionAlg.BLAKE2B, 8192)
+            assert pkg.hash_model(cfg, loaded).model_digest.data == porc.inplace_lattice(host, 8192), ("ckpt lattice", seed)
+        elif pick == 2:
+            cfg = pkg.HashConfig(C.MERKLE, S.COALESCED, pkg.CompressionAlg.from_name(alg), 8192)
+            assert pkg.hash_model(cfg, loaded).model_digest.data == porc.coalesced_merkle(alg, host, 8192), ("ckpt coalesced", seed)
+        else:
+            cfg = pkg.HashConfig(C.MERKLE, S.PER_LAYER, pkg.CompressionAlg.from_name(alg), 8192)
+            root, layers = porc.per_layer_merkle(alg, host, 8192)
+            res = pkg.hash_model(cfg, loaded)
+            assert res.model_digest.data == root and [d.data for d in res.layer_digests.values()] == list(layers), ("ckpt per-layer", seed)
+        del loaded
+    print(f"{case} random host-object cases")
