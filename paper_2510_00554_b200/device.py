@@ -405,6 +405,31 @@ def file_to_device(path, device: Optional[torch.device] = None, workers: int = 1
 ARENA_ALIGN = 256
 
 
+def file_ranges_to_device(fd: int, ranges: Sequence[Tuple[int, int]], device: Optional[torch.device] = None,
+                          workers: int = 1) -> List[torch.Tensor]:
+    """Byte ranges ``(offset, nbytes)`` of the open file ``fd`` as flat uint8 CUDA tensors (views of ONE arena), read
+    by the staging threads straight into the pinned ring: a rank of a sharded hash reads only the tensors it owns."""
+    device = device or require_cuda()
+    offs, pos = [], 0
+    for _, n in ranges:
+        offs.append(pos)
+        pos += -(-n // ARENA_ALIGN) * ARENA_ALIGN
+    arena = torch.empty(max(pos, 16), dtype=torch.uint8, device=device)
+    ring = StagingRing.get(staging_threads(workers))
+    stream = torch.cuda.current_stream()
+    with ring.lock:
+        w = RingWriter(ring, arena, stream)
+        try:
+            for (file_off, n), off in zip(ranges, offs):
+                if n:
+                    w.write_file(off, fd, file_off, n)
+            w.drain()
+        finally:
+            w.abandon()
+            stream.synchronize()
+    return [arena[off:off + n] for (_, n), off in zip(ranges, offs)]
+
+
 def _host_array(buf) -> np.ndarray:
     """Flat uint8 numpy view of a host buffer (bytes-like, numpy array or CPU tensor); zero copy when contiguous."""
     if isinstance(buf, torch.Tensor):

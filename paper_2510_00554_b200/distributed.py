@@ -255,7 +255,19 @@ def hash_model_sharded(cfg, model, rank: int, world: int, group=None):
     placeholder = torch.zeros(16, dtype=torch.uint8, device=dev)
     wanted = [i for i, (_, buf) in enumerate(model.entries)
               if (first[i] < b and first[i + 1] > a) or (isinstance(buf, torch.Tensor) and buf.device.type == "cuda")]
-    keep, w_ptrs, _ = _dev.device_spans([model.entries[i][1] for i in wanted], dev)
+    # file-backed tensors (load_model): this rank reads only the ranges it owns, file -> pinned ring -> its GPU
+    from .model import FileTensor
+
+    w_bufs = [model.entries[i][1] for i in wanted]
+    lazy = [j for j, buf in enumerate(w_bufs) if isinstance(buf, FileTensor) and buf.file._whole is None]
+    by_file = {}
+    for j in lazy:
+        by_file.setdefault(id(w_bufs[j].file), []).append(j)
+    for js in by_file.values():
+        got = _dev.file_ranges_to_device(w_bufs[js[0]].file.fd, [(w_bufs[j].offset, w_bufs[j].nbytes) for j in js], dev)
+        for j, t in zip(js, got):
+            w_bufs[j] = t
+    keep, w_ptrs, _ = _dev.device_spans(w_bufs, dev)
     ptrs = np.full(len(sizes), placeholder.data_ptr(), dtype=np.uint64)
     ptrs[np.asarray(wanted, dtype=np.int64)] = w_ptrs[:len(wanted)]
     ptrs[np.asarray(sizes) == 0] = 0

@@ -26,7 +26,7 @@ def _free_port() -> int:
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, sizes, q):
+def _worker(rank, world, port, sizes, q, ckpt=None):
     import torch.distributed as dist
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -44,6 +44,12 @@ def _worker(rank, world, port, sizes, q):
             entries = [(f"t{i}", torch.frombuffer(bytearray(t), dtype=torch.uint8).cuda() if (rank % 2 and t) else t)
                        for i, t in enumerate(tensors)]
             out[alg] = dd.hash_model_sharded(cfg, pkg.TensorMap(entries), rank, world).model_digest.data.hex()
+        if ckpt is not None:
+            # the same model as a checkpoint FILE: every rank preads only the tensors that own leaves of its shard run
+            loaded = pkg.load_model(ckpt)
+            cfg = pkg.HashConfig(pkg.Construction.MERKLE, pkg.Strategy.IN_PLACE, pkg.CompressionAlg.SHA256)
+            out["file"] = dd.hash_model_sharded(cfg, loaded, rank, world).model_digest.data.hex()
+            out["file_copied_to_host"] = loaded.entries[0][1].file._whole is not None
 
         n, declared = 999, [2, 3, 5, 7]
         rng = np.random.default_rng(17)
@@ -66,15 +72,18 @@ def _worker(rank, world, port, sizes, q):
 
 
 @pytest.mark.parametrize("world", [2, 3])
-def test_ranks_sharing_the_gpu_reproduce_single_gpu_digests(world, porc):
+def test_ranks_sharing_the_gpu_reproduce_single_gpu_digests(world, porc, tmp_path):
     import torch.multiprocessing as mp
+
+    import paper_2510_00554_b200 as pkg
 
     sizes = [8192 * 1500 + 77, 100, 0, 8192 * 2100, 31, 8192 * 900 + 4096, 5000]     # 4,501+ leaves: 5 shards of 1024
     tensors = inputs.model_tensors(91, sizes)
+    pkg.save_model(pkg.TensorMap([(f"t{i}", t) for i, t in enumerate(tensors)]), tmp_path / "ckpt.json")
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, sizes, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, sizes, q, str(tmp_path / "ckpt.json"))) for r in range(world)]
     for p in procs:
         p.start()
     results = {}
@@ -101,6 +110,8 @@ def test_ranks_sharing_the_gpu_reproduce_single_gpu_digests(world, porc):
         got = results[rank]
         for alg in ("sha256", "blake2b", "sha3-256"):
             assert got[alg] == porc.inplace_merkle(alg, tensors, 8192).hex(), (rank, alg)
+        assert got["file"] == porc.inplace_merkle("sha256", tensors, 8192).hex(), rank
+        assert got["file_copied_to_host"] is False, rank
         assert got["lattice"] == {k: (v[0].hex(), v[1]) for k, v in want_lat.items()}, rank
 
 
