@@ -10,7 +10,10 @@ to the root. `value` is whole-job throughput in GB/s (10^9 tensor bytes per seco
 resident in HBM; `e2e` is the same metric through the public `hash_model(cfg, TensorMap(host tensors))`
 call, host->device copies included. Every other BASELINE.json configuration rides along under "configs"
 (GPT-2 small SHA-256; BERT-large and VGG19 x {BLAKE2b, SHA3-256}; CIFAR10-shaped LtHash; the
-hellaswag-shaped pool of config 5), each with its own roofline and CPU reference.
+hellaswag-shaped pool of config 5), each with its own roofline and CPU reference. Beside `e2e` (page-locked host
+tensors) the line carries `e2e_pageable_host` (ordinary numpy arrays) and `e2e_checkpoint_file` (`load_model` +
+`hash_model` on a checkpoint file the bench writes to tmpfs); the dataset configurations add `process_batch_api`
+(the reference's loader loop), `manifest_api` (`digest_dataset` on manifest + shard file) and `streaming_api`.
 
 Parity is checked before any time is printed: the reference package
 (`oracle/_ref/sentinel`, staged by build()) hashes the D2H copy of the very bytes the GPU hashed; roots,
